@@ -1,0 +1,223 @@
+"""CPU oracle of the hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package. The product package
+``paper_2604_13191_b200`` never imports it, and this package never imports the product.
+
+This module is argument marshalling over ``oracle/oracle.c`` (plain C, pinned fp32 per
+``docs/PREDICATES.md``, exact ``__int128`` sums). See the C file's header for what is
+computed and how it is pinned.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+K_DEFAULT = 3
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc, -ffp-contract=off, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+             "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        f32p = C.POINTER(C.c_float)
+        i64p = C.POINTER(C.c_int64)
+        u64p = C.POINTER(C.c_uint64)
+        u8p = C.POINTER(C.c_uint8)
+        L.orc_create.restype = C.c_void_p
+        L.orc_create.argtypes = [C.c_uint32, f32p, C.c_int]
+        L.orc_destroy.argtypes = [C.c_void_p]
+        L.orc_set_window.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
+        L.orc_add_fibers.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64]
+        L.orc_add_triangles.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64]
+        L.orc_build.argtypes = [C.c_void_p, C.c_int]
+        L.orc_level_size.restype = C.c_uint64
+        L.orc_level_size.argtypes = [C.c_void_p, C.c_int]
+        L.orc_level_copy.argtypes = [C.c_void_p, C.c_int, u64p, i64p, f32p, f32p, u8p, i64p, f32p]
+        L.orc_morton.restype = C.c_uint64
+        L.orc_morton.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+        L.orc_unmorton.argtypes = [C.c_uint64] + [C.POINTER(C.c_uint32)] * 3
+        L.orc_grid.argtypes = [f32p, C.c_uint32, f32p, f32p]
+        L.orc_fiber_eval.argtypes = [f32p, f32p, C.c_float, C.c_int64, C.c_int64, C.c_int64, f32p]
+        L.orc_tri_sat.argtypes = [f32p, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_tri_area.restype = C.c_float
+        L.orc_tri_area.argtypes = [f32p, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_theta.argtypes = [f32p, f32p]
+        L.orc_sggxh.argtypes = [C.c_int, i64p, C.c_int, i64p]
+        L.orc_sigma.argtypes = [i64p, f32p]
+        L.orc_distance.restype = C.c_float
+        L.orc_distance.argtypes = [i64p, i64p]
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _i64(a):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a, a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise OracleError(f"{what} failed with oracle status {rc}")
+
+
+class Oracle:
+    """Plain CPU voxelizer + LoD builder (docs/PREDICATES.md §1-§9)."""
+
+    def __init__(self, grid_res: int, bbox, k: int = K_DEFAULT):
+        bb, p = _f32(np.asarray(bbox, dtype=np.float32).reshape(6))
+        self._bb = bb
+        self.k = int(k)
+        self.grid_res = int(grid_res)
+        self._h = lib().orc_create(int(grid_res), p, int(k))
+        if not self._h:
+            raise OracleError("orc_create rejected (grid_res, bbox, k)")
+
+    def close(self):
+        if self._h:
+            lib().orc_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_window(self, level: int, cell: int):
+        _check(lib().orc_set_window(self._h, int(level), int(cell)), "set_window")
+
+    def add_fibers(self, segments, radii):
+        s, sp = _f32(np.asarray(segments).reshape(-1, 6))
+        r, rp = _f32(np.asarray(radii).reshape(-1))
+        assert s.shape[0] == r.shape[0]
+        _check(lib().orc_add_fibers(self._h, sp, rp, s.shape[0]), "add_fibers")
+
+    def add_triangles(self, tris, dirs=None):
+        t, tp = _f32(np.asarray(tris).reshape(-1, 9))
+        if dirs is None:
+            dp = None
+        else:
+            d, dp = _f32(np.asarray(dirs).reshape(-1, 3))
+            assert d.shape[0] == t.shape[0]
+        _check(lib().orc_add_triangles(self._h, tp, dp, t.shape[0]), "add_triangles")
+
+    def build(self, levels: int = 0):
+        _check(lib().orc_build(self._h, int(levels)), "build")
+
+    def level(self, l: int) -> dict:
+        n = int(lib().orc_level_size(self._h, int(l)))
+        k = self.k
+        out = dict(
+            key=np.zeros(n, np.uint64), acc=np.zeros((n, 7), np.int64),
+            mass=np.zeros(n, np.float32), m6=np.zeros((n, 6), np.float32),
+            ncl=np.zeros(n, np.uint8), cl_acc=np.zeros((n, k, 7), np.int64),
+            cl=np.zeros((n, k, 7), np.float32))
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        _check(lib().orc_level_copy(self._h, int(l), P(out["key"], C.c_uint64), P(out["acc"], C.c_int64),
+                                    P(out["mass"], C.c_float), P(out["m6"], C.c_float),
+                                    P(out["ncl"], C.c_uint8), P(out["cl_acc"], C.c_int64),
+                                    P(out["cl"], C.c_float)), "level_copy")
+        return out
+
+
+# ----------------------------------------------------------------- unit entries
+
+def morton(i, j, k) -> int:
+    return int(lib().orc_morton(int(i), int(j), int(k)))
+
+
+def unmorton(key):
+    a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    lib().orc_unmorton(int(key), C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
+
+
+def grid(bbox, n, p):
+    bb, bp = _f32(np.asarray(bbox).reshape(6))
+    pp, ppp = _f32(np.asarray(p).reshape(3))
+    out = np.zeros(3, np.float32)
+    lib().orc_grid(bp, int(n), ppp, out.ctypes.data_as(C.POINTER(C.c_float)))
+    return out
+
+
+def fiber_eval(a, b, rg, i, j, k):
+    """Grid-space segment a->b, grid radius rg, voxel (i,j,k) -> (is_key, l_r)."""
+    A, ap = _f32(np.asarray(a).reshape(3))
+    B, bp = _f32(np.asarray(b).reshape(3))
+    ell = C.c_float(0)
+    key = lib().orc_fiber_eval(ap, bp, C.c_float(rg), int(i), int(j), int(k), C.byref(ell))
+    return bool(key), float(np.float32(ell.value))
+
+
+def tri_sat(g, i, j, k) -> bool:
+    G, gp = _f32(np.asarray(g).reshape(9))
+    return bool(lib().orc_tri_sat(gp, int(i), int(j), int(k)))
+
+
+def tri_area(g, i, j, k) -> float:
+    G, gp = _f32(np.asarray(g).reshape(9))
+    return float(np.float32(lib().orc_tri_area(gp, int(i), int(j), int(k))))
+
+
+def theta():
+    t = np.zeros((32, 3), np.float32)
+    c = np.zeros((32, 6), np.float32)
+    lib().orc_theta(t.ctypes.data_as(C.POINTER(C.c_float)), c.ctypes.data_as(C.POINTER(C.c_float)))
+    return t, c
+
+
+def sggxh(acc, k=K_DEFAULT):
+    """acc: (n,7) int64 cluster accumulators -> (m,7) kept clusters."""
+    a, ap = _i64(np.asarray(acc).reshape(-1, 7))
+    out = np.zeros((k, 7), np.int64)
+    m = lib().orc_sggxh(a.shape[0], ap, int(k), out.ctypes.data_as(C.POINTER(C.c_int64)))
+    if m < 0:
+        raise OracleError(f"sggxh status {m}")
+    return out[:m]
+
+
+def sigma(acc7):
+    a, ap = _i64(np.asarray(acc7).reshape(7))
+    s = np.zeros(32, np.float32)
+    lib().orc_sigma(ap, s.ctypes.data_as(C.POINTER(C.c_float)))
+    return s
+
+
+def distance(a7, b7) -> float:
+    a, ap = _i64(np.asarray(a7).reshape(7))
+    b, bp = _i64(np.asarray(b7).reshape(7))
+    return float(np.float32(lib().orc_distance(ap, bp)))
+
+
+Q = 2.0 ** 32
+
+
+def acc_from_float(w, m6):
+    """Helper for tests: quantise (w, M6) floats to int64 accumulators exactly as §8."""
+    v = np.concatenate([[w], m6]).astype(np.float32)
+    return np.rint((v * np.float32(Q)).astype(np.float32).astype(np.float64)).astype(np.int64)

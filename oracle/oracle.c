@@ -1,0 +1,811 @@
+/*
+ * oracle/oracle.c -- the CPU ORACLE of the hot path. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library. The product path (paper_2604_13191_b200/) never imports,
+ * links or executes anything under oracle/, and this file shares no code, header,
+ * table or constant generator with it.
+ *
+ * What it computes (paper: "Fast Voxelization and Level of Detail for Microgeometry
+ * Rendering", arXiv 2604.13191; P:n = PAPER.md line n, S:n = SPEC.md line n):
+ *   - sparse voxelization of fiber segments and triangles into a Morton-keyed grid
+ *     (P:164-170 normalisation, P:190-198 block test, P:242-248 gathering),
+ *   - per-voxel density mass and SGGX second moment M (moment form),
+ *   - the 2x2x2 LoD pyramid with SGGX-H clustering per parent.
+ * Formula by formula it follows docs/PREDICATES.md (section numbers "§n" below), which
+ * pins every floating-point operation (IEEE binary32, no FMA: compile with
+ * -ffp-contract=off and without -ffast-math) so that integer decisions (keys, merge
+ * argmins) are taken in the kernel's precision on both sides, and every sum of
+ * contributions is an exact integer sum (__int128 here).
+ *
+ * It is deliberately plain and slow: per primitive it enumerates every candidate voxel,
+ * evaluates the predicate, appends (key, quantised contribution) records, then sorts
+ * the records by key (qsort) and sums each run. SGGX-H recomputes every sigma and the
+ * full distance matrix after every merge.
+ *
+ * Parity pins (tests/test_oracle_*.py): closed forms (axis-aligned rectangle key
+ * counts, straight-fiber key sets and lengths), fp64 shadows, exact-rational SAT,
+ * brute force over all N^3 voxels, conservation laws, SPEC worked examples
+ * (tests/golden/). "Parity unpinned": the choice of the fiber
+ * weight l_r and of the sigma-distance have no printed value in the paper to match.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __int128 i128;
+
+#define ORC_OK 0
+#define ORC_ERR_ARG -1
+#define ORC_ERR_OOM -2
+#define ORC_ERR_OVERFLOW -3
+#define ORC_ERR_LEVEL -4
+
+#define MAX_LEVELS 14
+#define MAX_K 8
+
+/* ------------------------------------------------------------------ small helpers */
+
+static float fminf_(float a, float b) { return a < b ? a : b; }
+static float fmaxf_(float a, float b) { return a > b ? a : b; }
+
+/* §8: q(x) = llrint(fl(x * 2^32)) */
+static int64_t q32(float x) {
+    float y = x * 4294967296.0f;
+    return llrintf(y);
+}
+
+/* §8: fp32 output = fl((float)acc * 2^-32); acc must fit int64 (checked by caller). */
+static float deq32(i128 acc) {
+    float f = (float)(int64_t)acc;
+    return f * 2.3283064365386963e-10f; /* 2^-32, exact */
+}
+
+static int fits64(i128 v) { return v >= (i128)INT64_MIN && v <= (i128)INT64_MAX; }
+
+/* §2 Morton key, x in bit 0 */
+uint64_t orc_morton(uint32_t i, uint32_t j, uint32_t k) {
+    uint64_t key = 0;
+    for (int b = 0; b < 21; b++) {
+        key |= (uint64_t)((i >> b) & 1u) << (3 * b);
+        key |= (uint64_t)((j >> b) & 1u) << (3 * b + 1);
+        key |= (uint64_t)((k >> b) & 1u) << (3 * b + 2);
+    }
+    return key;
+}
+
+void orc_unmorton(uint64_t key, uint32_t* i, uint32_t* j, uint32_t* k) {
+    uint32_t x = 0, y = 0, z = 0;
+    for (int b = 0; b < 21; b++) {
+        x |= (uint32_t)((key >> (3 * b)) & 1u) << b;
+        y |= (uint32_t)((key >> (3 * b + 1)) & 1u) << b;
+        z |= (uint32_t)((key >> (3 * b + 2)) & 1u) << b;
+    }
+    *i = x; *j = y; *k = z;
+}
+
+/* ------------------------------------------------------------------ §1 grid transform */
+
+typedef struct {
+    uint32_t N;
+    float bmin[3];
+    float E;
+    float Nf;
+} grid_t;
+
+static int grid_init(grid_t* g, uint32_t N, const float bbox[6]) {
+    if (N < 2 || N > 8192 || (N & (N - 1))) return ORC_ERR_ARG;
+    float e[3];
+    for (int a = 0; a < 3; a++) {
+        if (!isfinite(bbox[a]) || !isfinite(bbox[3 + a])) return ORC_ERR_ARG;
+        e[a] = bbox[3 + a] - bbox[a];
+        if (!(e[a] > 0.0f)) return ORC_ERR_ARG;
+        g->bmin[a] = bbox[a];
+    }
+    g->E = fmaxf_(fmaxf_(e[0], e[1]), e[2]);
+    g->N = N;
+    g->Nf = (float)N;
+    return ORC_OK;
+}
+
+static float grid_coord(const grid_t* g, int a, float p) {
+    float t = p - g->bmin[a];
+    t = t / g->E;
+    return t * g->Nf;
+}
+
+static float grid_len(const grid_t* g, float r) {
+    float t = r / g->E;
+    return t * g->Nf;
+}
+
+void orc_grid(const float bbox[6], uint32_t N, const float p[3], float out[3]) {
+    grid_t g;
+    if (grid_init(&g, N, bbox) != ORC_OK) { out[0] = out[1] = out[2] = NAN; return; }
+    for (int a = 0; a < 3; a++) out[a] = grid_coord(&g, a, p[a]);
+}
+
+/* ------------------------------------------------------------------ §4 fiber predicate */
+
+typedef struct {
+    float a[3];      /* grid-space start */
+    float d[3];      /* fl(b - a) */
+    float w[3];      /* fl(d*d) */
+    float iota[3];   /* fl(1/d) for moving axes */
+    int moving[3];
+    float r2;        /* fl(rg*rg) */
+    float len;       /* |d| */
+} fiber_t;
+
+static void fiber_setup(fiber_t* f, const float a[3], const float b[3], float rg) {
+    for (int ax = 0; ax < 3; ax++) {
+        f->a[ax] = a[ax];
+        f->d[ax] = b[ax] - a[ax];
+        f->w[ax] = f->d[ax] * f->d[ax];
+        f->moving[ax] = f->w[ax] > 0.0f;
+        f->iota[ax] = f->moving[ax] ? 1.0f / f->d[ax] : 0.0f;
+    }
+    f->r2 = rg * rg;
+    float s = f->w[0] + f->w[1];
+    s = s + f->w[2];
+    f->len = sqrtf(s);
+}
+
+/* Returns 1 iff voxel (i,j,k) is a key of the capsule; then *ell = l_r (§4). */
+static int fiber_eval(const fiber_t* f, int64_t i, int64_t j, int64_t k, float* ell) {
+    const float lo[3] = {(float)i, (float)j, (float)k};
+    const float hi[3] = {(float)(i + 1), (float)(j + 1), (float)(k + 1)};
+    float u[3] = {0, 0, 0}, v[3] = {0, 0, 0};
+    float Wu[3] = {0, 0, 0}, Wuu[3] = {0, 0, 0}, Wv[3] = {0, 0, 0}, Wvv[3] = {0, 0, 0};
+    float C0 = 0.0f;
+    float bp[8];
+    int nbp = 0;
+    bp[nbp++] = 0.0f;
+    for (int ax = 0; ax < 3; ax++) {
+        if (f->moving[ax]) {
+            float t1 = (lo[ax] - f->a[ax]) * f->iota[ax];
+            float t2 = (hi[ax] - f->a[ax]) * f->iota[ax];
+            u[ax] = fminf_(t1, t2);
+            v[ax] = fmaxf_(t1, t2);
+            Wu[ax] = f->w[ax] * u[ax];
+            Wuu[ax] = Wu[ax] * u[ax];
+            Wv[ax] = f->w[ax] * v[ax];
+            Wvv[ax] = Wv[ax] * v[ax];
+            if (u[ax] > 0.0f && u[ax] < 1.0f) bp[nbp++] = u[ax];
+            if (v[ax] > 0.0f && v[ax] < 1.0f) bp[nbp++] = v[ax];
+        } else {
+            float c = 0.0f;
+            if (f->a[ax] < lo[ax]) c = lo[ax] - f->a[ax];
+            else if (f->a[ax] > hi[ax]) c = f->a[ax] - hi[ax];
+            C0 = C0 + c * c;
+        }
+    }
+    /* sort the interior breakpoints (indices 1..nbp-1) ascending; then append 1 */
+    for (int x = 2; x < nbp; x++) {
+        float key = bp[x];
+        int y = x - 1;
+        while (y >= 1 && bp[y] > key) { bp[y + 1] = bp[y]; y--; }
+        bp[y + 1] = key;
+    }
+    bp[nbp++] = 1.0f;
+
+    int found = 0;
+    float ta = 0.0f, tb = 0.0f;
+    for (int m = 0; m + 1 < nbp; m++) {
+        float L = bp[m], H = bp[m + 1];
+        float A = 0.0f, B = 0.0f, C = C0;
+        for (int ax = 0; ax < 3; ax++) {
+            if (!f->moving[ax]) continue;
+            if (u[ax] >= H) { A = A + f->w[ax]; B = B + Wu[ax]; C = C + Wuu[ax]; }
+            else if (v[ax] <= L) { A = A + f->w[ax]; B = B + Wv[ax]; C = C + Wvv[ax]; }
+        }
+        float lo_m, hi_m;
+        if (A == 0.0f) {
+            if (!(C <= f->r2)) continue;
+            lo_m = L; hi_m = H;
+        } else {
+            float Cr = C - f->r2;
+            float D = B * B - A * Cr;   /* two fl products then one fl difference */
+            if (D < 0.0f) continue;
+            float s = sqrtf(D);
+            float t1 = (B - s) / A;
+            float t2 = (B + s) / A;
+            lo_m = fmaxf_(t1, L);
+            hi_m = fminf_(t2, H);
+            if (!(lo_m <= hi_m)) continue;
+        }
+        if (!found) { ta = lo_m; tb = hi_m; found = 1; }
+        else { ta = fminf_(ta, lo_m); tb = fmaxf_(tb, hi_m); }
+    }
+    if (!found) return 0;
+    *ell = f->len * (tb - ta);
+    return 1;
+}
+
+/* Unit entry for tests: grid-space endpoints a, b and grid radius rg. */
+int orc_fiber_eval(const float a[3], const float b[3], float rg, int64_t i, int64_t j, int64_t k,
+                   float* ell) {
+    fiber_t f;
+    fiber_setup(&f, a, b, rg);
+    float e = 0.0f;
+    int key = fiber_eval(&f, i, j, k, &e);
+    *ell = e;
+    return key;
+}
+
+/* ------------------------------------------------------------------ §6 triangle SAT */
+
+static void cross3(const float f[3], const float g[3], float out[3]) {
+    out[0] = f[1] * g[2] - f[2] * g[1];
+    out[1] = f[2] * g[0] - f[0] * g[2];
+    out[2] = f[0] * g[1] - f[1] * g[0];
+}
+
+static int sep3(float p0, float p1, float p2, float rad) {
+    float mn = fminf_(fminf_(p0, p1), p2);
+    float mx = fmaxf_(fmaxf_(p0, p1), p2);
+    return mn > rad || mx < -rad;
+}
+
+static int tri_sat(const float g[9], int64_t i, int64_t j, int64_t k) {
+    const float h = 0.5f;
+    const float c[3] = {(float)i + 0.5f, (float)j + 0.5f, (float)k + 0.5f};
+    float v[3][3], e[3][3];
+    for (int m = 0; m < 3; m++)
+        for (int ax = 0; ax < 3; ax++) v[m][ax] = g[3 * m + ax] - c[ax];
+    for (int ax = 0; ax < 3; ax++) {
+        e[0][ax] = v[1][ax] - v[0][ax];
+        e[1][ax] = v[2][ax] - v[1][ax];
+        e[2][ax] = v[0][ax] - v[2][ax];
+    }
+    for (int q = 0; q < 3; q++) {
+        const float ex = e[q][0], ey = e[q][1], ez = e[q][2];
+        const float fx = fabsf(ex), fy = fabsf(ey), fz = fabsf(ez);
+        float p[3], rad;
+        /* X axis */
+        for (int m = 0; m < 3; m++) p[m] = ez * v[m][1] - ey * v[m][2];
+        rad = fz * h + fy * h;
+        if (sep3(p[0], p[1], p[2], rad)) return 0;
+        /* Y axis */
+        for (int m = 0; m < 3; m++) p[m] = ex * v[m][2] - ez * v[m][0];
+        rad = fz * h + fx * h;
+        if (sep3(p[0], p[1], p[2], rad)) return 0;
+        /* Z axis */
+        for (int m = 0; m < 3; m++) p[m] = ey * v[m][0] - ex * v[m][1];
+        rad = fy * h + fx * h;
+        if (sep3(p[0], p[1], p[2], rad)) return 0;
+    }
+    for (int ax = 0; ax < 3; ax++) {
+        float mn = fminf_(fminf_(v[0][ax], v[1][ax]), v[2][ax]);
+        float mx = fmaxf_(fmaxf_(v[0][ax], v[1][ax]), v[2][ax]);
+        if (mn > h || mx < -h) return 0;
+    }
+    float n[3], vmin[3], vmax[3];
+    cross3(e[0], e[1], n);
+    for (int ax = 0; ax < 3; ax++) {
+        if (n[ax] > 0.0f) { vmin[ax] = -h - v[0][ax]; vmax[ax] = h - v[0][ax]; }
+        else { vmin[ax] = h - v[0][ax]; vmax[ax] = -h - v[0][ax]; }
+    }
+    float dmin = n[0] * vmin[0] + n[1] * vmin[1];
+    dmin = dmin + n[2] * vmin[2];
+    if (dmin > 0.0f) return 0;
+    float dmax = n[0] * vmax[0] + n[1] * vmax[1];
+    dmax = dmax + n[2] * vmax[2];
+    if (dmax < 0.0f) return 0;
+    return 1;
+}
+
+int orc_tri_sat(const float g[9], int64_t i, int64_t j, int64_t k) { return tri_sat(g, i, j, k); }
+
+/* ------------------------------------------------------------------ §7 clipped area */
+
+#define MAXPOLY 12
+
+static int clip_plane(float in[][3], int n, float out[][3], int ax, float c, int upper) {
+    int m_out = 0;
+    for (int m = 0; m < n; m++) {
+        const float* cur = in[m];
+        const float* prev = in[(m + n - 1) % n];
+        int cin = upper ? (cur[ax] < c) : (cur[ax] >= c);
+        int pin = upper ? (prev[ax] < c) : (prev[ax] >= c);
+        if (cin != pin) {
+            /* I(prev, cur) */
+            float s = (c - prev[ax]) / (cur[ax] - prev[ax]);
+            for (int b = 0; b < 3; b++) {
+                if (b == ax) out[m_out][b] = c;
+                else out[m_out][b] = prev[b] + s * (cur[b] - prev[b]);
+            }
+            m_out++;
+        }
+        if (cin) {
+            for (int b = 0; b < 3; b++) out[m_out][b] = cur[b];
+            m_out++;
+        }
+    }
+    return m_out;
+}
+
+static float tri_area_in(const float g[9], int64_t i, int64_t j, int64_t k) {
+    float P[MAXPOLY][3], Q[MAXPOLY][3];
+    for (int m = 0; m < 3; m++)
+        for (int ax = 0; ax < 3; ax++) P[m][ax] = g[3 * m + ax];
+    int n = 3;
+    const float lo[3] = {(float)i, (float)j, (float)k};
+    const float hi[3] = {(float)(i + 1), (float)(j + 1), (float)(k + 1)};
+    for (int ax = 0; ax < 3; ax++) {
+        n = clip_plane(P, n, Q, ax, lo[ax], 0);
+        if (n < 3) return 0.0f;
+        n = clip_plane(Q, n, P, ax, hi[ax], 1);
+        if (n < 3) return 0.0f;
+    }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    for (int m = 1; m + 1 < n; m++) {
+        float e1[3], e2[3], cr[3];
+        for (int ax = 0; ax < 3; ax++) {
+            e1[ax] = P[m][ax] - P[0][ax];
+            e2[ax] = P[m + 1][ax] - P[0][ax];
+        }
+        cross3(e1, e2, cr);
+        for (int ax = 0; ax < 3; ax++) acc[ax] = acc[ax] + cr[ax];
+    }
+    float s = acc[0] * acc[0] + acc[1] * acc[1];
+    s = s + acc[2] * acc[2];
+    return 0.5f * sqrtf(s);
+}
+
+float orc_tri_area(const float g[9], int64_t i, int64_t j, int64_t k) { return tri_area_in(g, i, j, k); }
+
+/* ------------------------------------------------------------------ records, levels */
+
+typedef struct {
+    uint64_t key;
+    int64_t q[7];
+} rec_t;
+
+typedef struct {
+    uint64_t n;
+    uint64_t* key;
+    i128* acc;      /* [n][7] */
+    uint8_t* ncl;   /* [n] */
+    i128* cl;       /* [n][K][7] */
+} level_t;
+
+typedef struct {
+    grid_t g;
+    int logN;
+    int K;
+    /* emission window: a Morton cell (level wl, index wc) as a voxel box */
+    int64_t wlo[3], whi[3];   /* inclusive voxel range */
+    rec_t* recs;
+    size_t nrec, cap;
+    int built;                /* levels built (-1: nothing) */
+    level_t lv[MAX_LEVELS];
+} orc_ctx;
+
+static int push_rec(orc_ctx* c, uint64_t key, const int64_t q[7]) {
+    if (c->nrec == c->cap) {
+        size_t nc = c->cap ? 2 * c->cap : 1024;
+        rec_t* r = (rec_t*)realloc(c->recs, nc * sizeof(rec_t));
+        if (!r) return ORC_ERR_OOM;
+        c->recs = r;
+        c->cap = nc;
+    }
+    c->recs[c->nrec].key = key;
+    memcpy(c->recs[c->nrec].q, q, sizeof(int64_t) * 7);
+    c->nrec++;
+    return ORC_OK;
+}
+
+static void free_levels(orc_ctx* c) {
+    for (int l = 0; l < MAX_LEVELS; l++) {
+        free(c->lv[l].key); free(c->lv[l].acc); free(c->lv[l].ncl); free(c->lv[l].cl);
+        memset(&c->lv[l], 0, sizeof(level_t));
+    }
+    c->built = -1;
+}
+
+orc_ctx* orc_create(uint32_t N, const float bbox[6], int K) {
+    orc_ctx* c = (orc_ctx*)calloc(1, sizeof(orc_ctx));
+    if (!c) return NULL;
+    if (grid_init(&c->g, N, bbox) != ORC_OK || K < 1 || K > MAX_K) { free(c); return NULL; }
+    c->logN = 0;
+    while ((1u << c->logN) < N) c->logN++;
+    c->K = K;
+    for (int a = 0; a < 3; a++) { c->wlo[a] = 0; c->whi[a] = (int64_t)N - 1; }
+    c->built = -1;
+    return c;
+}
+
+void orc_destroy(orc_ctx* c) {
+    if (!c) return;
+    free_levels(c);
+    free(c->recs);
+    free(c);
+}
+
+/* Restrict emission to the voxels of Morton cell `cell` at level `wl` (windowed parity).
+ * Segment normalisation S_p still runs over all keys (§5), so in-window values are the
+ * same as in a full run. */
+int orc_set_window(orc_ctx* c, int wl, uint64_t cell) {
+    if (wl < 0 || wl > c->logN) return ORC_ERR_ARG;
+    uint32_t i, j, k;
+    orc_unmorton(cell, &i, &j, &k);
+    int64_t sz = (int64_t)1 << wl;
+    int64_t o[3] = {(int64_t)i * sz, (int64_t)j * sz, (int64_t)k * sz};
+    for (int a = 0; a < 3; a++) {
+        if (o[a] + sz > (int64_t)c->g.N) return ORC_ERR_ARG;
+        c->wlo[a] = o[a];
+        c->whi[a] = o[a] + sz - 1;
+    }
+    return ORC_OK;
+}
+
+static int in_window(const orc_ctx* c, int64_t i, int64_t j, int64_t k) {
+    return i >= c->wlo[0] && i <= c->whi[0] && j >= c->wlo[1] && j <= c->whi[1] &&
+           k >= c->wlo[2] && k <= c->whi[2];
+}
+
+/* §3: integer candidate range [ceil(lo)-1, floor(hi)] of one axis */
+static void cand_range(float lo, float hi, int64_t* c0, int64_t* c1) {
+    *c0 = (int64_t)ceilf(lo) - 1;
+    *c1 = (int64_t)floorf(hi);
+}
+
+/* §4, §5 */
+int orc_add_fibers(orc_ctx* c, const float* seg, const float* radii, uint64_t S) {
+    const float PI_F = 3.14159274101257324f; /* 0x40490FDB */
+    c->built = -1;
+    for (uint64_t p = 0; p < S; p++) {
+        const float* s = seg + 6 * p;
+        float r = radii[p];
+        for (int q = 0; q < 6; q++) if (!isfinite(s[q])) return ORC_ERR_ARG;
+        if (!isfinite(r) || r < 0.0f) return ORC_ERR_ARG;
+        float a[3], b[3];
+        for (int ax = 0; ax < 3; ax++) {
+            a[ax] = grid_coord(&c->g, ax, s[ax]);
+            b[ax] = grid_coord(&c->g, ax, s[3 + ax]);
+        }
+        float rg = grid_len(&c->g, r);
+        int64_t u0[3], u1[3];   /* unclamped candidate range */
+        int culled = 0;
+        for (int ax = 0; ax < 3; ax++) {
+            float lo = fminf_(a[ax], b[ax]) - rg;
+            float hi = fmaxf_(a[ax], b[ax]) + rg;
+            if (!(hi >= -1.0f) || !(lo <= (float)c->g.N + 1.0f)) { culled = 1; break; }
+            if (hi - lo > 16777216.0f) return ORC_ERR_ARG; /* > 2^24 candidates (§3) */
+            cand_range(lo, hi, &u0[ax], &u1[ax]);
+            int64_t e0 = u0[ax] < c->wlo[ax] ? c->wlo[ax] : u0[ax];
+            int64_t e1 = u1[ax] > c->whi[ax] ? c->whi[ax] : u1[ax];
+            if (e0 > e1) culled = 1;
+        }
+        if (culled) continue;
+        uint64_t ncand = (uint64_t)(u1[0] - u0[0] + 1) * (uint64_t)(u1[1] - u0[1] + 1) *
+                         (uint64_t)(u1[2] - u0[2] + 1);
+        if (ncand > (1ull << 24)) return ORC_ERR_ARG;
+        fiber_t f;
+        fiber_setup(&f, a, b, rg);
+        /* first pass: every key in the unclamped range -> S_acc */
+        float* ells = (float*)malloc(sizeof(float) * ncand);
+        uint8_t* iskey = (uint8_t*)malloc(ncand);
+        if (!ells || !iskey) { free(ells); free(iskey); return ORC_ERR_OOM; }
+        i128 Sacc = 0;
+        uint64_t idx = 0;
+        for (int64_t k = u0[2]; k <= u1[2]; k++)
+            for (int64_t j = u0[1]; j <= u1[1]; j++)
+                for (int64_t i = u0[0]; i <= u1[0]; i++, idx++) {
+                    float ell = 0.0f;
+                    iskey[idx] = (uint8_t)fiber_eval(&f, i, j, k, &ell);
+                    ells[idx] = ell;
+                    if (iskey[idx]) Sacc += q32(ell);
+                }
+        if (!fits64(Sacc)) { free(ells); free(iskey); return ORC_ERR_OVERFLOW; }
+        float Sp = deq32(Sacc);
+        float mp = PI_F * rg;
+        mp = mp * rg;
+        mp = mp * f.len;
+        float fp = Sacc > 0 ? mp / Sp : 0.0f;
+        float t[3];
+        for (int ax = 0; ax < 3; ax++) t[ax] = f.len > 0.0f ? f.d[ax] / f.len : 0.0f;
+        /* second pass: contributions of in-grid, in-window keys */
+        idx = 0;
+        for (int64_t k = u0[2]; k <= u1[2]; k++)
+            for (int64_t j = u0[1]; j <= u1[1]; j++)
+                for (int64_t i = u0[0]; i <= u1[0]; i++, idx++) {
+                    if (!iskey[idx] || !in_window(c, i, j, k)) continue;
+                    float mass = fp * ells[idx];
+                    int64_t q[7];
+                    q[0] = q32(mass);
+                    q[1] = q32((mass * t[0]) * t[0]);
+                    q[2] = q32((mass * t[1]) * t[1]);
+                    q[3] = q32((mass * t[2]) * t[2]);
+                    q[4] = q32((mass * t[0]) * t[1]);
+                    q[5] = q32((mass * t[0]) * t[2]);
+                    q[6] = q32((mass * t[1]) * t[2]);
+                    int rc = push_rec(c, orc_morton((uint32_t)i, (uint32_t)j, (uint32_t)k), q);
+                    if (rc) { free(ells); free(iskey); return rc; }
+                }
+        free(ells);
+        free(iskey);
+    }
+    return ORC_OK;
+}
+
+/* §6, §7 */
+int orc_add_triangles(orc_ctx* c, const float* tri, const float* dirs, uint64_t T) {
+    c->built = -1;
+    for (uint64_t t = 0; t < T; t++) {
+        const float* v = tri + 9 * t;
+        for (int q = 0; q < 9; q++) if (!isfinite(v[q])) return ORC_ERR_ARG;
+        float g[9];
+        for (int m = 0; m < 3; m++)
+            for (int ax = 0; ax < 3; ax++) g[3 * m + ax] = grid_coord(&c->g, ax, v[3 * m + ax]);
+        /* direction (face normal of the grid-space triangle, or the caller's dirs) */
+        float w[3];
+        if (dirs) {
+            for (int ax = 0; ax < 3; ax++) {
+                w[ax] = dirs[3 * t + ax];
+                if (!isfinite(w[ax])) return ORC_ERR_ARG;
+            }
+        } else {
+            float f1[3], f2[3];
+            for (int ax = 0; ax < 3; ax++) { f1[ax] = g[3 + ax] - g[ax]; f2[ax] = g[6 + ax] - g[3 + ax]; }
+            cross3(f1, f2, w);
+        }
+        float nn = w[0] * w[0] + w[1] * w[1];
+        nn = nn + w[2] * w[2];
+        float nrm = sqrtf(nn);
+        if (dirs && !(nrm > 0.0f)) return ORC_ERR_ARG;
+        float dh[3];
+        for (int ax = 0; ax < 3; ax++) dh[ax] = nrm > 0.0f ? w[ax] / nrm : 0.0f;
+        int64_t e0[3], e1[3];
+        int culled = 0;
+        for (int ax = 0; ax < 3; ax++) {
+            float lo = fminf_(fminf_(g[ax], g[3 + ax]), g[6 + ax]);
+            float hi = fmaxf_(fmaxf_(g[ax], g[3 + ax]), g[6 + ax]);
+            if (!(hi >= -1.0f) || !(lo <= (float)c->g.N + 1.0f)) { culled = 1; break; }
+            cand_range(lo, hi, &e0[ax], &e1[ax]);
+            if (e0[ax] < c->wlo[ax]) e0[ax] = c->wlo[ax];
+            if (e1[ax] > c->whi[ax]) e1[ax] = c->whi[ax];
+            if (e0[ax] > e1[ax]) culled = 1;
+        }
+        if (culled) continue;
+        for (int64_t k = e0[2]; k <= e1[2]; k++)
+            for (int64_t j = e0[1]; j <= e1[1]; j++)
+                for (int64_t i = e0[0]; i <= e1[0]; i++) {
+                    if (!tri_sat(g, i, j, k)) continue;
+                    float A = tri_area_in(g, i, j, k);
+                    float mass = 1.0f * A;
+                    int64_t q[7];
+                    q[0] = q32(mass);
+                    q[1] = q32((mass * dh[0]) * dh[0]);
+                    q[2] = q32((mass * dh[1]) * dh[1]);
+                    q[3] = q32((mass * dh[2]) * dh[2]);
+                    q[4] = q32((mass * dh[0]) * dh[1]);
+                    q[5] = q32((mass * dh[0]) * dh[2]);
+                    q[6] = q32((mass * dh[1]) * dh[2]);
+                    int rc = push_rec(c, orc_morton((uint32_t)i, (uint32_t)j, (uint32_t)k), q);
+                    if (rc) return rc;
+                }
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ §9 SGGX-H */
+
+static void theta_table(float theta[32][3], float coef[32][6]) {
+    const double PI_D = 3.14159265358979323846;
+    const double ga = PI_D * (3.0 - sqrt(5.0));
+    for (int k = 0; k < 32; k++) {
+        double z = 1.0 - (k + 0.5) / 32.0;
+        double rho = sqrt(1.0 - z * z);
+        double phi = k * ga;
+        theta[k][0] = (float)(rho * cos(phi));
+        theta[k][1] = (float)(rho * sin(phi));
+        theta[k][2] = (float)z;
+        double x = theta[k][0], y = theta[k][1], zz = theta[k][2];
+        coef[k][0] = (float)(x * x);
+        coef[k][1] = (float)(y * y);
+        coef[k][2] = (float)(zz * zz);
+        coef[k][3] = (float)(2.0 * x * y);
+        coef[k][4] = (float)(2.0 * x * zz);
+        coef[k][5] = (float)(2.0 * y * zz);
+    }
+}
+
+void orc_theta(float* theta, float* coef) {
+    float t[32][3], c[32][6];
+    theta_table(t, c);
+    memcpy(theta, t, sizeof(t));
+    memcpy(coef, c, sizeof(c));
+}
+
+/* sigma_k of one cluster from its accumulators (w, Mxx, Myy, Mzz, Mxy, Mxz, Myz) */
+static void cluster_sigma(const i128 acc[7], const float coef[32][6], float sig[32]) {
+    float wf = deq32(acc[0]);
+    float S[6];
+    for (int e = 0; e < 6; e++) S[e] = deq32(acc[1 + e]) / wf;
+    for (int k = 0; k < 32; k++) {
+        float q = coef[k][0] * S[0];
+        for (int e = 1; e < 6; e++) q = q + coef[k][e] * S[e];
+        sig[k] = sqrtf(fmaxf_(q, 0.0f));
+    }
+}
+
+static float sigma_dist(const float si[32], const float sj[32]) {
+    float s[32];
+    for (int k = 0; k < 32; k++) s[k] = fabsf(si[k] - sj[k]);
+    for (int h = 16; h >= 1; h >>= 1)
+        for (int l = 0; l < h; l++) s[l] = s[l] + s[l + h];
+    return s[0];
+}
+
+/* SGGX-H on n clusters (in order), down to K. Clusters are [n][7] i128, modified in
+ * place; returns the number kept. P:383-387: D_{L-1} = (D_L \ {S_i,S_j}) U S_n. */
+static int sggxh(i128 (*cl)[7], int n, int K, const float coef[32][6]) {
+    float sig[8 * MAX_K][32];
+    while (n > K) {
+        for (int c = 0; c < n; c++) cluster_sigma(cl[c], coef, sig[c]);
+        int bi = 0, bj = 1;
+        float best = 0.0f;
+        int have = 0;
+        for (int i = 0; i < n; i++)
+            for (int j = i + 1; j < n; j++) {
+                float d = sigma_dist(sig[i], sig[j]);
+                if (!have || d < best) { best = d; bi = i; bj = j; have = 1; }
+            }
+        for (int e = 0; e < 7; e++) cl[bi][e] += cl[bj][e];
+        for (int c = bj; c + 1 < n; c++) memcpy(cl[c], cl[c + 1], sizeof(cl[c]));
+        n--;
+    }
+    return n;
+}
+
+/* Unit entry: n clusters of int64 accumulators -> out [K][7]; returns ncl. */
+int orc_sggxh(int n, const int64_t* acc, int K, int64_t* out) {
+    if (n < 0 || n > 8 * MAX_K || K < 1 || K > MAX_K) return ORC_ERR_ARG;
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    i128 cl[8 * MAX_K][7];
+    int m = 0;
+    for (int c = 0; c < n; c++) {
+        if (acc[7 * c] == 0) continue; /* w = 0 clusters are dropped */
+        for (int e = 0; e < 7; e++) cl[m][e] = acc[7 * c + e];
+        m++;
+    }
+    if (m > K) m = sggxh(cl, m, K, coef);
+    for (int c = 0; c < m; c++)
+        for (int e = 0; e < 7; e++) {
+            if (!fits64(cl[c][e])) return ORC_ERR_OVERFLOW;
+            out[7 * c + e] = (int64_t)cl[c][e];
+        }
+    return m;
+}
+
+void orc_sigma(const int64_t acc[7], float sig[32]) {
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    i128 a[7];
+    for (int e = 0; e < 7; e++) a[e] = acc[e];
+    cluster_sigma(a, coef, sig);
+}
+
+float orc_distance(const int64_t a[7], const int64_t b[7]) {
+    float sa[32], sb[32];
+    orc_sigma(a, sa);
+    orc_sigma(b, sb);
+    return sigma_dist(sa, sb);
+}
+
+static int cmp_rec(const void* x, const void* y) {
+    uint64_t a = ((const rec_t*)x)->key, b = ((const rec_t*)y)->key;
+    return a < b ? -1 : a > b;
+}
+
+/* Leaf (§8, §9 level 0) then levels 1..levels (§9). */
+int orc_build(orc_ctx* c, int levels) {
+    if (levels < 0 || levels > c->logN) return ORC_ERR_LEVEL;
+    free_levels(c);
+    const int K = c->K;
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    /* level 0: sort records by key and sum each run exactly */
+    qsort(c->recs, c->nrec, sizeof(rec_t), cmp_rec);
+    uint64_t V = 0;
+    for (size_t r = 0; r < c->nrec; r++)
+        if (r == 0 || c->recs[r].key != c->recs[r - 1].key) V++;
+    level_t* L0 = &c->lv[0];
+    L0->n = V;
+    L0->key = (uint64_t*)malloc(sizeof(uint64_t) * (V ? V : 1));
+    L0->acc = (i128*)calloc((V ? V : 1) * 7, sizeof(i128));
+    L0->ncl = (uint8_t*)calloc(V ? V : 1, 1);
+    L0->cl = (i128*)calloc((V ? V : 1) * K * 7, sizeof(i128));
+    if (!L0->key || !L0->acc || !L0->ncl || !L0->cl) return ORC_ERR_OOM;
+    int64_t v = -1;
+    for (size_t r = 0; r < c->nrec; r++) {
+        if (r == 0 || c->recs[r].key != c->recs[r - 1].key) { v++; L0->key[v] = c->recs[r].key; }
+        for (int e = 0; e < 7; e++) L0->acc[7 * v + e] += c->recs[r].q[e];
+    }
+    for (uint64_t x = 0; x < V; x++) {
+        for (int e = 0; e < 7; e++)
+            if (!fits64(L0->acc[7 * x + e])) return ORC_ERR_OVERFLOW;
+        if (L0->acc[7 * x] > 0) {
+            L0->ncl[x] = 1;
+            for (int e = 0; e < 7; e++) L0->cl[(size_t)x * K * 7 + e] = L0->acc[7 * x + e];
+        }
+    }
+    c->built = 0;
+    for (int l = 1; l <= levels; l++) {
+        level_t* Cc = &c->lv[l - 1];
+        level_t* P = &c->lv[l];
+        uint64_t nP = 0;
+        for (uint64_t x = 0; x < Cc->n; x++)
+            if (x == 0 || (Cc->key[x] >> 3) != (Cc->key[x - 1] >> 3)) nP++;
+        P->n = nP;
+        P->key = (uint64_t*)malloc(sizeof(uint64_t) * (nP ? nP : 1));
+        P->acc = (i128*)calloc((nP ? nP : 1) * 7, sizeof(i128));
+        P->ncl = (uint8_t*)calloc(nP ? nP : 1, 1);
+        P->cl = (i128*)calloc((nP ? nP : 1) * K * 7, sizeof(i128));
+        if (!P->key || !P->acc || !P->ncl || !P->cl) return ORC_ERR_OOM;
+        uint64_t x = 0, p = 0;
+        while (x < Cc->n) {
+            uint64_t pk = Cc->key[x] >> 3;
+            i128 list[8 * MAX_K][7];
+            int n = 0;
+            P->key[p] = pk;
+            while (x < Cc->n && (Cc->key[x] >> 3) == pk) {
+                for (int e = 0; e < 7; e++) P->acc[7 * p + e] += Cc->acc[7 * x + e];
+                for (int q = 0; q < Cc->ncl[x]; q++) {
+                    const i128* src = &Cc->cl[((size_t)x * K + q) * 7];
+                    if (src[0] == 0) continue;
+                    for (int e = 0; e < 7; e++) list[n][e] = src[e];
+                    n++;
+                }
+                x++;
+            }
+            if (n > K) n = sggxh(list, n, K, coef);
+            P->ncl[p] = (uint8_t)n;
+            for (int q = 0; q < n; q++)
+                for (int e = 0; e < 7; e++) {
+                    if (!fits64(list[q][e])) return ORC_ERR_OVERFLOW;
+                    P->cl[((size_t)p * K + q) * 7 + e] = list[q][e];
+                }
+            for (int e = 0; e < 7; e++)
+                if (!fits64(P->acc[7 * p + e])) return ORC_ERR_OVERFLOW;
+            p++;
+        }
+        c->built = l;
+    }
+    return ORC_OK;
+}
+
+uint64_t orc_level_size(const orc_ctx* c, int l) {
+    if (l < 0 || l > c->built) return 0;
+    return c->lv[l].n;
+}
+
+/* Copy level l out: keys, int64 accumulators [n][7], fp32 mass/m6, ncl, cluster
+ * accumulators [n][K][7] and fp32 clusters [n][K][7] (unused slots zero). */
+int orc_level_copy(const orc_ctx* c, int l, uint64_t* key, int64_t* acc, float* mass, float* m6,
+                   uint8_t* ncl, int64_t* clacc, float* cl) {
+    if (l < 0 || l > c->built) return ORC_ERR_LEVEL;
+    const level_t* L = &c->lv[l];
+    const int K = c->K;
+    for (uint64_t x = 0; x < L->n; x++) {
+        if (key) key[x] = L->key[x];
+        for (int e = 0; e < 7; e++) {
+            i128 a = L->acc[7 * x + e];
+            if (acc) acc[7 * x + e] = (int64_t)a;
+            if (e == 0) { if (mass) mass[x] = deq32(a); }
+            else if (m6) m6[6 * x + e - 1] = deq32(a);
+        }
+        if (ncl) ncl[x] = L->ncl[x];
+        for (int q = 0; q < K; q++)
+            for (int e = 0; e < 7; e++) {
+                i128 a = L->cl[((size_t)x * K + q) * 7 + e];
+                if (clacc) clacc[((size_t)x * K + q) * 7 + e] = (int64_t)a;
+                if (cl) cl[((size_t)x * K + q) * 7 + e] = q < L->ncl[x] ? deq32(a) : 0.0f;
+            }
+    }
+    return ORC_OK;
+}
