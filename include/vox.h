@@ -1,0 +1,158 @@
+/*
+ * vox.h -- C ABI of the B200-native sparse voxelizer + SGGX-H LoD builder.
+ *
+ * Method: "Fast Voxelization and Level of Detail for Microgeometry Rendering"
+ * (arXiv 2604.13191). P:n = line n of the paper's LaTeX; docs/PREDICATES.md
+ * (§n) pins every operation; DESIGN.md lists the readings (Dn) of the paper.
+ *
+ * Conventions (all entry points):
+ *   - C linkage, no exceptions cross the ABI; every call returns a vox_status.
+ *   - Device pointers are CUDA device (or managed) memory, fp32 contiguous, 4-byte
+ *     aligned (16-byte alignment is faster, not required). They are caller-owned and must
+ *     stay valid until the call's work completes on the ctx stream (vox_sync).
+ *   - Every call is ordered on the ctx stream (vox_options.stream, a cudaStream_t; NULL =
+ *     the legacy default stream). The only internal host synchronisations are the small
+ *     device->host reads that size allocations (documented per call).
+ *   - Outputs are owned by the ctx. Views returned by vox_read_level stay valid until the
+ *     next mutating call on the ctx or vox_destroy.
+ *   - A ctx is not thread-safe; distinct ctxs are independent.
+ *   - Results are bit-identical for identical (grid_res, bbox, options, multiset of
+ *     primitives), independent of primitive order, batch splits, run and GPU count
+ *     (exact integer accumulation, PREDICATES §8).
+ */
+#ifndef VOX_H
+#define VOX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vox_ctx vox_ctx;
+
+typedef enum {
+    VOX_OK = 0,
+    VOX_ERR_INVALID_ARG = 1,     /* bad argument, NaN/Inf input, negative radius, zero dir */
+    VOX_ERR_DEGENERATE_BBOX = 2, /* non-finite bbox or b_max <= b_min on an axis */
+    VOX_ERR_STATE = 3,           /* call not allowed in the ctx's current state */
+    VOX_ERR_OOM = 4,             /* device allocation failed */
+    VOX_ERR_CAPACITY = 5,        /* estimated bytes exceed vox_options.max_bytes */
+    VOX_ERR_CUDA = 6,            /* a CUDA runtime error (see vox_last_error) */
+    VOX_ERR_LEVEL = 7,           /* level out of range or not built yet */
+    VOX_ERR_COMM = 8             /* export/import buffer malformed or too small */
+} vox_status;
+
+/* Zero-initialised = defaults. */
+typedef struct {
+    void* stream;          /* cudaStream_t for every call (NULL = default stream) */
+    int rank;              /* Morton-range shard of this ctx, 0..world-1 (default 0) */
+    int world;             /* number of shards (default 1 = unsharded) */
+    int top_depth;         /* T: sharding/binning by Morton prefixes of 3T bits; 0 = min(4, log2 N) */
+    uint32_t k;            /* max SGGX lobes kept per voxel, 1..8 (default 3) */
+    uint32_t n_slices;     /* slice directions of the SGGX-H distance: 32 only (default 32) */
+    uint64_t max_bytes;    /* cap on scratch+output device bytes per call (0 = no cap) */
+    int profile;           /* 1 = record per-stage CUDA events (vox_stats times) */
+} vox_options;
+
+/* Level view. Level 0 (leaves): ncl and cl are NULL; a leaf holds exactly one lobe
+ * (mass, M) iff mass > 0. */
+typedef struct {
+    uint64_t n;            /* voxels in the level (this rank's part for local levels) */
+    const uint64_t* key;   /* [n] Morton keys of the level (key >> 3l of leaf keys), ascending */
+    const float* mass;     /* [n] density mass (PREDICATES §5, §7; D9) */
+    const float* m6;       /* [n][6] second moment M: xx, yy, zz, xy, xz, yz (SGGX S = M / mass) */
+    const uint8_t* ncl;    /* [n] number of SGGX-H lobes kept (<= k), or NULL for level 0 */
+    const float* cl;       /* [n][k][7] lobes (w, M6); slots >= ncl are zero; NULL for level 0 */
+    const int64_t* acc;    /* [n][7] exact fixed-point accumulators (quantum 2^-32) */
+} vox_level_view;
+
+typedef struct {
+    uint64_t segments;     /* primitives read by the last voxelize call */
+    uint64_t candidates;   /* in-grid, in-shard candidate voxels (upper bound on pairs) */
+    uint64_t pairs;        /* (key, contribution) pairs emitted by the last call */
+    uint64_t voxels;       /* leaf voxels after the last call */
+    uint32_t top_depth;    /* T in use */
+    uint64_t cell_lo, cell_hi; /* this rank's top-cell range [lo, hi) */
+    /* accumulated device milliseconds per stage since the last vox_stats_reset (profile=1) */
+    double ms_bound, ms_emit, ms_sort, ms_reduce, ms_merge, ms_lod_scan, ms_lod, ms_total_vox, ms_total_lod;
+    uint64_t launches;     /* kernels launched by the library since the last reset */
+} vox_stats;
+
+/* Create a ctx for an N^3 grid over the cubic extent of bbox (D3).
+ * grid_res: power of two in [2, 8192] (D27) else VOX_ERR_INVALID_ARG.
+ * bbox: host float[6] = min xyz, max xyz; must be finite with max > min per axis
+ * (else VOX_ERR_DEGENERATE_BBOX). opt: host pointer or NULL (defaults). No device
+ * allocation happens here. */
+vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], const vox_options* opt);
+
+/* Voxelize S fiber segments (capsules; PREDICATES §3-§5, north star).
+ * segments: device float[S][2][3] world-space endpoints; radii: device float[S] (>= 0).
+ * Accumulates into the leaf level (D19). S = 0 is a no-op VOX_OK (D26).
+ * NaN/Inf coordinates, negative radii or a segment with > 2^24 candidate voxels ->
+ * VOX_ERR_INVALID_ARG (detected on the device; the leaf level is unchanged).
+ * Host syncs: 2 small reads (per-top-cell candidate counts; emitted pair count). */
+vox_status vox_voxelize_fibers(vox_ctx* ctx, const float* segments, const float* radii, uint64_t S);
+
+/* Voxelize T triangles (PREDICATES §6-§7). tris: device float[T][3][3] world
+ * vertices (soup); dirs: device float[T][3] per-triangle direction (tangent mode,
+ * P:183) or NULL for face normals. A zero-norm dir -> VOX_ERR_INVALID_ARG. */
+vox_status vox_voxelize_triangles(vox_ctx* ctx, const float* tris, const float* dirs, uint64_t T);
+
+/* Same as the two calls above with HOST input pointers (pinned memory is fastest): the
+ * host->device copies run on the ctx stream inside the call. */
+vox_status vox_voxelize_fibers_host(vox_ctx* ctx, const float* segments, const float* radii, uint64_t S);
+vox_status vox_voxelize_triangles_host(vox_ctx* ctx, const float* tris, const float* dirs, uint64_t T);
+
+/* Build levels 1..levels of the 2x2x2 Morton pyramid with SGGX-H per parent
+ * (PREDICATES §9). levels <= log2(grid_res) else VOX_ERR_LEVEL. Levels already
+ * built are kept; voxelize_* afterwards returns VOX_ERR_STATE. Sharded ctx (world > 1):
+ * builds at most up to level log2(N) - T until vox_import_level(log2(N) - T) has been
+ * called (query vox_built_levels). Host syncs: one 8-byte read per level. */
+vox_status vox_build_lod(vox_ctx* ctx, uint32_t levels);
+
+/* Highest level available for reading (0 after create). */
+vox_status vox_built_levels(vox_ctx* ctx, uint32_t* out);
+
+/* Borrowed view of a level (see vox_level_view). level > built -> VOX_ERR_LEVEL. */
+vox_status vox_read_level(vox_ctx* ctx, uint32_t level, vox_level_view* out);
+
+/* Copy a level into caller-owned buffers (device or host; any pointer may be NULL):
+ * key [n], mass [n], m6 [n][6], ncl [n], cl [n][k][7]. Level 0 copies ncl = (mass > 0)
+ * and cl = (mass, M) in slot 0. Synchronises the ctx stream when a buffer is host memory. */
+vox_status vox_copy_level(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
+                          uint8_t* ncl, float* cl);
+
+/* Copy a level's exact accumulators acc [n][7] (int64, quantum 2^-32; device or host). */
+vox_status vox_copy_level_acc(vox_ctx* ctx, uint32_t level, int64_t* acc);
+
+/* Multi-GPU (Morton-range shards). A level's records are fixed-size:
+ * key u64, acc i64[7], ncl u64 (low byte), lobe accumulators i64[k][7]  ->  72 + 56k bytes.
+ * export: dev_buf == NULL -> *bytes = required size; else writes the records of this rank
+ * (device memory, *bytes must be >= required; on return *bytes = bytes written).
+ * import: replaces `level` with the concatenation of all ranks' records in rank order
+ * (ascending keys), which must be level log2(N) - T; afterwards vox_build_lod can build
+ * the top levels redundantly on every rank. Bad sizes or unsorted keys -> VOX_ERR_COMM. */
+vox_status vox_export_level(vox_ctx* ctx, uint32_t level, void* dev_buf, uint64_t* bytes);
+vox_status vox_import_level(vox_ctx* ctx, uint32_t level, const void* dev_buf, uint64_t bytes);
+
+/* Deterministic work-balanced partition of 8^T top cells over `world` ranks (host only,
+ * no GPU needed): bounds[r] = first cell of rank r, bounds[world] = ncells; rank r owns
+ * [bounds[r], bounds[r+1]). weights[c] = candidate voxels in cell c. The first voxelize
+ * call of a sharded ctx computes this from its candidate counts and freezes it. */
+vox_status vox_plan_shards(const uint64_t* weights, uint64_t ncells, int world, uint64_t* bounds);
+
+/* Host copy of the SGGX-H slice table (PREDICATES §9): theta [32][3], coef [32][6]. */
+vox_status vox_theta_table(float* theta, float* coef);
+
+vox_status vox_stats_get(vox_ctx* ctx, vox_stats* out);   /* synchronises the stream */
+vox_status vox_stats_reset(vox_ctx* ctx);
+vox_status vox_sync(vox_ctx* ctx);
+const char* vox_status_str(vox_status s);
+const char* vox_last_error(vox_ctx* ctx);
+void vox_destroy(vox_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOX_H */

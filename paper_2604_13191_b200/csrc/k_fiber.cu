@@ -1,0 +1,335 @@
+// k_fiber.cu -- fiber segments: cull/bin (k_fiber_bound) and capsule-box overlap + emit
+// (k_fiber_emit). docs/PREDICATES.md §1, §3, §4, §5 (north star: fiber-capsule-box test
+// emitting (Morton key, contribution) pairs; P:190-198 block test as a conservative cull;
+// P:224-228 t-uniform curve sampling whose continuous limit is the ball-touch length).
+#include "vox_internal.cuh"
+
+namespace vox {
+
+struct SegGeom {
+    float a[3], b[3], rg;
+    bool culled;
+    bool too_many;
+    int64_t u0[3], u1[3];   // unclamped candidate range (§3)
+    int64_t e0[3], e1[3];   // emission range (clamped to the grid)
+};
+
+// §1 + §3 for one segment (shared by the bound and emit kernels).
+__device__ __forceinline__ void seg_geom(const GridXf& g, const float* s, float r, SegGeom& G) {
+    for (int ax = 0; ax < 3; ax++) {
+        G.a[ax] = to_grid(g, ax, s[ax]);
+        G.b[ax] = to_grid(g, ax, s[3 + ax]);
+    }
+    G.rg = to_grid_len(g, r);
+    G.culled = false;
+    G.too_many = false;
+    const float Nhi = g.Nf + 1.0f;
+    for (int ax = 0; ax < 3; ax++) {
+        float lo = pmin(G.a[ax], G.b[ax]) - G.rg;
+        float hi = pmax(G.a[ax], G.b[ax]) + G.rg;
+        if (!(hi >= -1.0f) || !(lo <= Nhi)) { G.culled = true; return; }
+        if (hi - lo > 16777216.0f) { G.too_many = true; G.culled = true; return; }
+        G.u0[ax] = (int64_t)ceilf(lo) - 1;
+        G.u1[ax] = (int64_t)floorf(hi);
+        G.e0[ax] = G.u0[ax] < 0 ? 0 : G.u0[ax];
+        G.e1[ax] = G.u1[ax] > g.N - 1 ? g.N - 1 : G.u1[ax];
+        if (G.e0[ax] > G.e1[ax]) G.culled = true;
+    }
+    if (!G.culled) {
+        uint64_t n = (uint64_t)(G.u1[0] - G.u0[0] + 1) * (uint64_t)(G.u1[1] - G.u0[1] + 1) *
+                     (uint64_t)(G.u1[2] - G.u0[2] + 1);
+        if (n > (1ull << 24)) { G.too_many = true; G.culled = true; }
+    }
+}
+
+// Adds the clamped candidate count of box [e0,e1] to each top cell it overlaps (cell edge
+// = 2^s voxels). Used for capacity (exact upper bound on pairs per cell) and sharding.
+__device__ __forceinline__ void add_cells(const int64_t* e0, const int64_t* e1, int s,
+                                          unsigned long long* cellW) {
+    const int64_t c0x = e0[0] >> s, c1x = e1[0] >> s;
+    const int64_t c0y = e0[1] >> s, c1y = e1[1] >> s;
+    const int64_t c0z = e0[2] >> s, c1z = e1[2] >> s;
+    for (int64_t cz = c0z; cz <= c1z; cz++) {
+        int64_t nz = min(e1[2], ((cz + 1) << s) - 1) - max(e0[2], cz << s) + 1;
+        for (int64_t cy = c0y; cy <= c1y; cy++) {
+            int64_t ny = min(e1[1], ((cy + 1) << s) - 1) - max(e0[1], cy << s) + 1;
+            for (int64_t cx = c0x; cx <= c1x; cx++) {
+                int64_t nx = min(e1[0], ((cx + 1) << s) - 1) - max(e0[0], cx << s) + 1;
+                atomicAdd(&cellW[morton3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz)],
+                          (unsigned long long)(nx * ny * nz));
+            }
+        }
+    }
+}
+
+__global__ void k_fiber_bound(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S,
+                              GridXf g, int cell_shift, unsigned long long* __restrict__ cellW,
+                              unsigned* __restrict__ flags) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < S;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        float s[6];
+        for (int q = 0; q < 6; q++) s[q] = seg[6 * p + q];
+        const float r = rad[p];
+        bool bad = false;
+        for (int q = 0; q < 6; q++) bad |= !isfinite(s[q]);
+        bad |= !isfinite(r);
+        if (bad) { atomicOr(flags, VOX_EFLAG_NONFINITE); continue; }
+        if (r < 0.0f) { atomicOr(flags, VOX_EFLAG_NEG_RADIUS); continue; }
+        SegGeom G;
+        seg_geom(g, s, r, G);
+        if (G.too_many) { atomicOr(flags, VOX_EFLAG_TOO_MANY_CAND); continue; }
+        if (G.culled) continue;
+        add_cells(G.e0, G.e1, cell_shift, cellW);
+    }
+}
+
+// ---------------------------------------------------------------- §4 capsule-box predicate
+
+struct Fib {
+    float a[3], w[3], iota[3];
+    float r2, len;
+    unsigned moving;   // bit ax set iff w_ax > 0
+};
+
+// Sorting network for 6 values (ascending); values outside (0,1) were replaced by 2.
+__device__ __forceinline__ void cswap(float& x, float& y) {
+    float lo = pmin(x, y), hi = pmax(x, y);
+    x = lo; y = hi;
+}
+
+// Returns true iff voxel (i,j,k) is a key; ell = l_r. Pinned sequence of PREDICATES §4.
+__device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, int64_t k, float& ell) {
+    const float lo[3] = {(float)i, (float)j, (float)k};
+    const float hi[3] = {(float)(i + 1), (float)(j + 1), (float)(k + 1)};
+    float u[3], v[3], Wu[3], Wuu[3], Wv[3], Wvv[3];
+    float C0 = 0.0f;
+    float bp[6];
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+        if (f.moving & (1u << ax)) {
+            float t1 = (lo[ax] - f.a[ax]) * f.iota[ax];
+            float t2 = (hi[ax] - f.a[ax]) * f.iota[ax];
+            u[ax] = pmin(t1, t2);
+            v[ax] = pmax(t1, t2);
+            Wu[ax] = f.w[ax] * u[ax];
+            Wuu[ax] = Wu[ax] * u[ax];
+            Wv[ax] = f.w[ax] * v[ax];
+            Wvv[ax] = Wv[ax] * v[ax];
+            bp[2 * ax] = (u[ax] > 0.0f && u[ax] < 1.0f) ? u[ax] : 2.0f;
+            bp[2 * ax + 1] = (v[ax] > 0.0f && v[ax] < 1.0f) ? v[ax] : 2.0f;
+        } else {
+            u[ax] = v[ax] = Wu[ax] = Wuu[ax] = Wv[ax] = Wvv[ax] = 0.0f;
+            float c = 0.0f;
+            if (f.a[ax] < lo[ax]) c = lo[ax] - f.a[ax];
+            else if (f.a[ax] > hi[ax]) c = f.a[ax] - hi[ax];
+            C0 = C0 + c * c;
+            bp[2 * ax] = bp[2 * ax + 1] = 2.0f;
+        }
+    }
+    // optimal 12-comparator network for 6 inputs
+    cswap(bp[1], bp[2]); cswap(bp[4], bp[5]); cswap(bp[0], bp[2]); cswap(bp[3], bp[5]);
+    cswap(bp[0], bp[1]); cswap(bp[3], bp[4]); cswap(bp[1], bp[4]); cswap(bp[0], bp[3]);
+    cswap(bp[2], bp[5]); cswap(bp[1], bp[3]); cswap(bp[2], bp[4]); cswap(bp[2], bp[3]);
+    int m = 0;
+#pragma unroll
+    for (int q = 0; q < 6; q++) m += bp[q] < 1.0f;   // interior breakpoints
+
+    bool found = false;
+    float ta = 0.0f, tb = 0.0f;
+#pragma unroll
+    for (int p = 0; p < 7; p++) {
+        if (p > m) break;
+        const float L = p == 0 ? 0.0f : bp[p - 1];
+        const float H = p < m ? bp[p] : 1.0f;
+        float A = 0.0f, B = 0.0f, C = C0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) {
+            if (!(f.moving & (1u << ax))) continue;
+            if (u[ax] >= H) { A = A + f.w[ax]; B = B + Wu[ax]; C = C + Wuu[ax]; }
+            else if (v[ax] <= L) { A = A + f.w[ax]; B = B + Wv[ax]; C = C + Wvv[ax]; }
+        }
+        float lo_m, hi_m;
+        if (A == 0.0f) {
+            if (!(C <= f.r2)) continue;
+            lo_m = L; hi_m = H;
+        } else {
+            float Cr = C - f.r2;
+            float D = B * B - A * Cr;
+            if (D < 0.0f) continue;
+            float s = sqrtf(D);
+            float t1 = (B - s) / A;
+            float t2 = (B + s) / A;
+            lo_m = pmax(t1, L);
+            hi_m = pmin(t2, H);
+            if (!(lo_m <= hi_m)) continue;
+        }
+        if (!found) { ta = lo_m; tb = hi_m; found = true; }
+        else { ta = pmin(ta, lo_m); tb = pmax(tb, hi_m); }
+    }
+    if (!found) return false;
+    ell = f.len * (tb - ta);
+    return true;
+}
+
+// ---------------------------------------------------------------- emit
+
+constexpr int EMIT_WARPS = 8;
+
+// One warp per batch of 32 consecutive segments. The batch's candidate voxels (the
+// unclamped AABB ranges, §3) are flattened and dealt round-robin to the 32 lanes, so every
+// lane evaluates one (segment, voxel) candidate per step whatever the segment sizes.
+// Keys add q(l_r) into the segment's exact S_acc (shared int64); in-grid, in-shard keys are
+// compacted with a warp ballot and appended to the pair stream with one atomic per warp step.
+__global__ void __launch_bounds__(EMIT_WARPS * 32)
+k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g, Shard sh,
+             uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab, uint64_t cap,
+             unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
+    __shared__ float s_f[EMIT_WARPS][12][32];
+    __shared__ int64_t s_u0[EMIT_WARPS][3][32];
+    __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
+    __shared__ uint32_t s_start[EMIT_WARPS][32];
+    __shared__ unsigned long long s_acc[EMIT_WARPS][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t nbatch = (S + 31) / 32;
+    const float PI_F = 3.14159274101257324f;   // 0x40490FDB
+    for (uint64_t batch = blockIdx.x * (uint64_t)EMIT_WARPS + wib; batch < nbatch;
+         batch += (uint64_t)gridDim.x * EMIT_WARPS) {
+        const uint64_t p = batch * 32 + lane;
+        uint32_t cnt = 0;
+        Fib f;
+        float d[3] = {0, 0, 0};
+        float rg = 0.0f;
+        if (p < S) {
+            float s[6];
+            for (int q = 0; q < 6; q++) s[q] = seg[6 * p + q];
+            SegGeom G;
+            seg_geom(g, s, rad[p], G);
+            rg = G.rg;
+            if (!G.culled) {
+                cnt = (uint32_t)((G.u1[0] - G.u0[0] + 1) * (G.u1[1] - G.u0[1] + 1) * (G.u1[2] - G.u0[2] + 1));
+                for (int ax = 0; ax < 3; ax++) s_u0[wib][ax][lane] = G.u0[ax];
+                s_ex[wib][0][lane] = (uint32_t)(G.u1[0] - G.u0[0] + 1);
+                s_ex[wib][1][lane] = (uint32_t)(G.u1[1] - G.u0[1] + 1);
+            }
+            f.moving = 0;
+            for (int ax = 0; ax < 3; ax++) {
+                f.a[ax] = G.a[ax];
+                d[ax] = G.b[ax] - G.a[ax];
+                f.w[ax] = d[ax] * d[ax];
+                if (f.w[ax] > 0.0f) { f.moving |= 1u << ax; f.iota[ax] = 1.0f / d[ax]; }
+                else f.iota[ax] = 0.0f;
+            }
+            f.r2 = rg * rg;
+            float ss = f.w[0] + f.w[1];
+            ss = ss + f.w[2];
+            f.len = sqrtf(ss);
+            for (int ax = 0; ax < 3; ax++) {
+                s_f[wib][ax][lane] = f.a[ax];
+                s_f[wib][3 + ax][lane] = f.w[ax];
+                s_f[wib][6 + ax][lane] = f.iota[ax];
+            }
+            s_f[wib][9][lane] = f.r2;
+            s_f[wib][10][lane] = __uint_as_float(f.moving);
+            s_f[wib][11][lane] = f.len;
+        }
+        // warp inclusive scan of the candidate counts
+        uint32_t incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_start[wib][lane] = incl - cnt;
+        s_acc[wib][lane] = 0ull;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            bool emit = false;
+            uint64_t mkey = 0, val = 0;
+            if (c < total) {
+                int o = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1)
+                    if (s_start[wib][o + step] <= c) o += step;
+                const uint32_t local = c - s_start[wib][o];
+                const uint32_t ex = s_ex[wib][0][o], ey = s_ex[wib][1][o];
+                const uint32_t t = local / ex;
+                const int64_t i = s_u0[wib][0][o] + (int64_t)(local - t * ex);
+                const int64_t j = s_u0[wib][1][o] + (int64_t)(t % ey);
+                const int64_t k = s_u0[wib][2][o] + (int64_t)(t / ey);
+                Fib fo;
+                for (int ax = 0; ax < 3; ax++) {
+                    fo.a[ax] = s_f[wib][ax][o];
+                    fo.w[ax] = s_f[wib][3 + ax][o];
+                    fo.iota[ax] = s_f[wib][6 + ax][o];
+                }
+                fo.r2 = s_f[wib][9][o];
+                fo.moving = __float_as_uint(s_f[wib][10][o]);
+                fo.len = s_f[wib][11][o];
+                float ell;
+                if (fiber_key(fo, i, j, k, ell)) {
+                    atomicAdd(&s_acc[wib][o], (unsigned long long)q32(ell));
+                    if (i >= 0 && j >= 0 && k >= 0 && i < g.N && j < g.N && k < g.N) {
+                        mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
+                        const uint64_t cell = mkey >> sh.shift;
+                        if (cell >= sh.cell_lo && cell < sh.cell_hi) {
+                            emit = true;
+                            val = (batch * 32 + o) | ((uint64_t)__float_as_uint(ell) << 32);
+                        }
+                    }
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, emit);
+            if (bal) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(cursor, (unsigned long long)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (emit) {
+                    const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                    if (pos < cap) { keys[pos] = mkey; vals[pos] = val; }
+                    else atomicOr(flags, VOX_EFLAG_OVERFLOW);
+                }
+            }
+        }
+        __syncwarp();
+        if (p < S) {
+            // §5 per-segment normalisation f_p = m_p / S_p and unit tangent
+            const long long Sacc = (long long)s_acc[wib][lane];
+            const float Sp = deq32(Sacc);
+            float mp = PI_F * rg;
+            mp = mp * rg;
+            mp = mp * f.len;
+            const float fp = Sacc > 0 ? mp / Sp : 0.0f;
+            float4 e;
+            e.x = f.len > 0.0f ? d[0] / f.len : 0.0f;
+            e.y = f.len > 0.0f ? d[1] / f.len : 0.0f;
+            e.z = f.len > 0.0f ? d[2] / f.len : 0.0f;
+            e.w = fp;
+            ptab[p] = e;
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_fiber_bound(vox_ctx* c, const float* seg, const float* rad, uint64_t S,
+                               unsigned long long* cellW, int T) {
+    const int threads = 256;
+    uint64_t blocks = (S + threads - 1) / threads;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    k_fiber_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(seg, rad, S, c->g, c->g.logN - T, cellW, c->d_flags);
+    c->st.launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh,
+                              uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap) {
+    const uint64_t nbatch = (S + 31) / 32;
+    uint64_t blocks = (nbatch + EMIT_WARPS - 1) / EMIT_WARPS;
+    if (blocks > (1ull << 30)) blocks = 1ull << 30;
+    k_fiber_emit<<<(unsigned)blocks, EMIT_WARPS * 32, 0, c->stream>>>(seg, rad, S, c->g, sh, keys, vals, ptab, cap,
+                                                                      c->d_counter, c->d_flags);
+    c->st.launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace vox

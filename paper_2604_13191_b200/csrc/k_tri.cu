@@ -1,0 +1,307 @@
+// k_tri.cu -- triangles: cull/bin (k_tri_bound) and separating-axis triangle-box test +
+// half-open clipped area emit (k_tri_emit). docs/PREDICATES.md §1, §3, §6, §7 (north star:
+// triangle-box SAT; P:225-228 area-weighted triangle sampling whose continuous limit is the
+// clipped area; P:179 face normals, P:183/P:549 tangent mode).
+#include "vox_internal.cuh"
+
+namespace vox {
+
+struct TriGeom {
+    float g[9];
+    bool culled;
+    int64_t e0[3], e1[3];
+};
+
+__device__ __forceinline__ void tri_geom(const GridXf& gx, const float* v, TriGeom& G) {
+    for (int m = 0; m < 3; m++)
+        for (int ax = 0; ax < 3; ax++) G.g[3 * m + ax] = to_grid(gx, ax, v[3 * m + ax]);
+    G.culled = false;
+    const float Nhi = gx.Nf + 1.0f;
+    for (int ax = 0; ax < 3; ax++) {
+        float lo = pmin(pmin(G.g[ax], G.g[3 + ax]), G.g[6 + ax]);
+        float hi = pmax(pmax(G.g[ax], G.g[3 + ax]), G.g[6 + ax]);
+        if (!(hi >= -1.0f) || !(lo <= Nhi)) { G.culled = true; return; }
+        int64_t c0 = (int64_t)ceilf(lo) - 1, c1 = (int64_t)floorf(hi);
+        G.e0[ax] = c0 < 0 ? 0 : c0;
+        G.e1[ax] = c1 > gx.N - 1 ? gx.N - 1 : c1;
+        if (G.e0[ax] > G.e1[ax]) G.culled = true;
+    }
+}
+
+__device__ __forceinline__ void cross3(const float* f, const float* g, float* o) {
+    o[0] = f[1] * g[2] - f[2] * g[1];
+    o[1] = f[2] * g[0] - f[0] * g[2];
+    o[2] = f[0] * g[1] - f[1] * g[0];
+}
+
+// §7 direction: face normal of the grid-space triangle or the caller's dir; returns nrm.
+__device__ __forceinline__ float tri_dir(const float* g, const float* dir, float* dh) {
+    float w[3];
+    if (dir) {
+        w[0] = dir[0]; w[1] = dir[1]; w[2] = dir[2];
+    } else {
+        float f1[3], f2[3];
+        for (int ax = 0; ax < 3; ax++) { f1[ax] = g[3 + ax] - g[ax]; f2[ax] = g[6 + ax] - g[3 + ax]; }
+        cross3(f1, f2, w);
+    }
+    float nn = w[0] * w[0] + w[1] * w[1];
+    nn = nn + w[2] * w[2];
+    const float nrm = sqrtf(nn);
+    for (int ax = 0; ax < 3; ax++) dh[ax] = nrm > 0.0f ? w[ax] / nrm : 0.0f;
+    return nrm;
+}
+
+__global__ void k_tri_bound(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx,
+                            int cell_shift, unsigned long long* __restrict__ cellW, unsigned* __restrict__ flags) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        float v[9];
+        bool bad = false;
+        for (int q = 0; q < 9; q++) { v[q] = tri[9 * t + q]; bad |= !isfinite(v[q]); }
+        if (dirs) {
+            float d[3] = {dirs[3 * t], dirs[3 * t + 1], dirs[3 * t + 2]};
+            for (int q = 0; q < 3; q++) bad |= !isfinite(d[q]);
+            if (!bad) {
+                float nn = d[0] * d[0] + d[1] * d[1];
+                nn = nn + d[2] * d[2];
+                if (!(sqrtf(nn) > 0.0f)) { atomicOr(flags, VOX_EFLAG_ZERO_DIR); continue; }
+            }
+        }
+        if (bad) { atomicOr(flags, VOX_EFLAG_NONFINITE); continue; }
+        TriGeom G;
+        tri_geom(gx, v, G);
+        if (G.culled) continue;
+        const int s = cell_shift;
+        for (int64_t cz = G.e0[2] >> s; cz <= G.e1[2] >> s; cz++) {
+            int64_t nz = min(G.e1[2], ((cz + 1) << s) - 1) - max(G.e0[2], cz << s) + 1;
+            for (int64_t cy = G.e0[1] >> s; cy <= G.e1[1] >> s; cy++) {
+                int64_t ny = min(G.e1[1], ((cy + 1) << s) - 1) - max(G.e0[1], cy << s) + 1;
+                for (int64_t cx = G.e0[0] >> s; cx <= G.e1[0] >> s; cx++) {
+                    int64_t nx = min(G.e1[0], ((cx + 1) << s) - 1) - max(G.e0[0], cx << s) + 1;
+                    atomicAdd(&cellW[morton3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz)],
+                              (unsigned long long)(nx * ny * nz));
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- §6 SAT (closed box)
+
+__device__ __forceinline__ bool sep3(float p0, float p1, float p2, float rad) {
+    const float mn = pmin(pmin(p0, p1), p2);
+    const float mx = pmax(pmax(p0, p1), p2);
+    return mn > rad || mx < -rad;
+}
+
+__device__ __forceinline__ bool tri_box_sat(const float* g, int64_t i, int64_t j, int64_t k) {
+    const float h = 0.5f;
+    const float c[3] = {(float)i + 0.5f, (float)j + 0.5f, (float)k + 0.5f};
+    float v[3][3], e[3][3];
+#pragma unroll
+    for (int m = 0; m < 3; m++)
+#pragma unroll
+        for (int ax = 0; ax < 3; ax++) v[m][ax] = g[3 * m + ax] - c[ax];
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+        e[0][ax] = v[1][ax] - v[0][ax];
+        e[1][ax] = v[2][ax] - v[1][ax];
+        e[2][ax] = v[0][ax] - v[2][ax];
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const float ex = e[q][0], ey = e[q][1], ez = e[q][2];
+        const float fx = fabsf(ex), fy = fabsf(ey), fz = fabsf(ez);
+        float p[3];
+        for (int m = 0; m < 3; m++) p[m] = ez * v[m][1] - ey * v[m][2];
+        if (sep3(p[0], p[1], p[2], fz * h + fy * h)) return false;
+        for (int m = 0; m < 3; m++) p[m] = ex * v[m][2] - ez * v[m][0];
+        if (sep3(p[0], p[1], p[2], fz * h + fx * h)) return false;
+        for (int m = 0; m < 3; m++) p[m] = ey * v[m][0] - ex * v[m][1];
+        if (sep3(p[0], p[1], p[2], fy * h + fx * h)) return false;
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+        const float mn = pmin(pmin(v[0][ax], v[1][ax]), v[2][ax]);
+        const float mx = pmax(pmax(v[0][ax], v[1][ax]), v[2][ax]);
+        if (mn > h || mx < -h) return false;
+    }
+    float n[3], vmin[3], vmax[3];
+    cross3(e[0], e[1], n);
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+        if (n[ax] > 0.0f) { vmin[ax] = -h - v[0][ax]; vmax[ax] = h - v[0][ax]; }
+        else { vmin[ax] = h - v[0][ax]; vmax[ax] = -h - v[0][ax]; }
+    }
+    float dmin = n[0] * vmin[0] + n[1] * vmin[1];
+    dmin = dmin + n[2] * vmin[2];
+    if (dmin > 0.0f) return false;
+    float dmax = n[0] * vmax[0] + n[1] * vmax[1];
+    dmax = dmax + n[2] * vmax[2];
+    return !(dmax < 0.0f);
+}
+
+// ---------------------------------------------------------------- §7 clipped area (half-open box)
+
+constexpr int MAXPOLY = 12;
+
+__device__ __forceinline__ int clip_one(const float (*in)[3], int n, float (*out)[3], int ax, float c, bool upper) {
+    int o = 0;
+    for (int m = 0; m < n; m++) {
+        const float* cur = in[m];
+        const float* prev = in[m == 0 ? n - 1 : m - 1];
+        const bool cin = upper ? (cur[ax] < c) : (cur[ax] >= c);
+        const bool pin = upper ? (prev[ax] < c) : (prev[ax] >= c);
+        if (cin != pin) {
+            const float s = (c - prev[ax]) / (cur[ax] - prev[ax]);
+            for (int b = 0; b < 3; b++) out[o][b] = (b == ax) ? c : prev[b] + s * (cur[b] - prev[b]);
+            o++;
+        }
+        if (cin) {
+            out[o][0] = cur[0]; out[o][1] = cur[1]; out[o][2] = cur[2];
+            o++;
+        }
+    }
+    return o;
+}
+
+__device__ float tri_clip_area(const float* g, int64_t i, int64_t j, int64_t k) {
+    float P[MAXPOLY][3], Q[MAXPOLY][3];
+    for (int m = 0; m < 3; m++)
+        for (int ax = 0; ax < 3; ax++) P[m][ax] = g[3 * m + ax];
+    int n = 3;
+    const float lo[3] = {(float)i, (float)j, (float)k};
+    const float hi[3] = {(float)(i + 1), (float)(j + 1), (float)(k + 1)};
+    for (int ax = 0; ax < 3; ax++) {
+        n = clip_one(P, n, Q, ax, lo[ax], false);
+        if (n < 3) return 0.0f;
+        n = clip_one(Q, n, P, ax, hi[ax], true);
+        if (n < 3) return 0.0f;
+    }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    for (int m = 1; m + 1 < n; m++) {
+        float e1[3], e2[3], cr[3];
+        for (int ax = 0; ax < 3; ax++) {
+            e1[ax] = P[m][ax] - P[0][ax];
+            e2[ax] = P[m + 1][ax] - P[0][ax];
+        }
+        cross3(e1, e2, cr);
+        for (int ax = 0; ax < 3; ax++) acc[ax] = acc[ax] + cr[ax];
+    }
+    float s = acc[0] * acc[0] + acc[1] * acc[1];
+    s = s + acc[2] * acc[2];
+    return 0.5f * sqrtf(s);
+}
+
+// ---------------------------------------------------------------- emit
+
+constexpr int TRI_WARPS = 4;
+
+// One warp per batch of 32 triangles; the batch's clamped candidate voxels are flattened
+// and dealt round-robin to the lanes (same scheme as k_fiber_emit). Keys (SAT) emit
+// (key, prim | area) pairs; the prim table holds (d_hat, f = 1).
+__global__ void __launch_bounds__(TRI_WARPS * 32)
+k_tri_emit(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx, Shard sh,
+           uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab, uint64_t cap,
+           unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
+    __shared__ float s_g[TRI_WARPS][9][32];
+    __shared__ int64_t s_e0[TRI_WARPS][3][32];
+    __shared__ uint32_t s_ex[TRI_WARPS][2][32];
+    __shared__ unsigned long long s_start[TRI_WARPS][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t nbatch = (T + 31) / 32;
+    for (uint64_t batch = blockIdx.x * (uint64_t)TRI_WARPS + wib; batch < nbatch;
+         batch += (uint64_t)gridDim.x * TRI_WARPS) {
+        const uint64_t t = batch * 32 + lane;
+        unsigned long long cnt = 0;
+        if (t < T) {
+            float v[9];
+            for (int q = 0; q < 9; q++) v[q] = tri[9 * t + q];
+            TriGeom G;
+            tri_geom(gx, v, G);
+            float dh[3];
+            tri_dir(G.g, dirs ? dirs + 3 * t : nullptr, dh);
+            ptab[t] = make_float4(dh[0], dh[1], dh[2], 1.0f);
+            if (!G.culled) {
+                cnt = (unsigned long long)(G.e1[0] - G.e0[0] + 1) * (unsigned long long)(G.e1[1] - G.e0[1] + 1) *
+                      (unsigned long long)(G.e1[2] - G.e0[2] + 1);
+                for (int ax = 0; ax < 3; ax++) s_e0[wib][ax][lane] = G.e0[ax];
+                s_ex[wib][0][lane] = (uint32_t)(G.e1[0] - G.e0[0] + 1);
+                s_ex[wib][1][lane] = (uint32_t)(G.e1[1] - G.e0[1] + 1);
+            }
+            for (int q = 0; q < 9; q++) s_g[wib][q][lane] = G.g[q];
+        }
+        unsigned long long incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_start[wib][lane] = incl - cnt;
+        const unsigned long long total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        for (unsigned long long c0 = 0; c0 < total; c0 += 32) {
+            const unsigned long long c = c0 + lane;
+            bool emit = false;
+            uint64_t mkey = 0, val = 0;
+            if (c < total) {
+                int o = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1)
+                    if (s_start[wib][o + step] <= c) o += step;
+                const unsigned long long local = c - s_start[wib][o];
+                const unsigned long long ex = s_ex[wib][0][o], ey = s_ex[wib][1][o];
+                const unsigned long long q = local / ex;
+                const int64_t i = s_e0[wib][0][o] + (int64_t)(local - q * ex);
+                const int64_t j = s_e0[wib][1][o] + (int64_t)(q % ey);
+                const int64_t k = s_e0[wib][2][o] + (int64_t)(q / ey);
+                float g[9];
+                for (int m = 0; m < 9; m++) g[m] = s_g[wib][m][o];
+                if (tri_box_sat(g, i, j, k)) {
+                    mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
+                    const uint64_t cell = mkey >> sh.shift;
+                    if (cell >= sh.cell_lo && cell < sh.cell_hi) {
+                        const float A = tri_clip_area(g, i, j, k);
+                        emit = true;
+                        val = (batch * 32 + o) | ((uint64_t)__float_as_uint(A) << 32);
+                    }
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, emit);
+            if (bal) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(cursor, (unsigned long long)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (emit) {
+                    const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                    if (pos < cap) { keys[pos] = mkey; vals[pos] = val; }
+                    else atomicOr(flags, VOX_EFLAG_OVERFLOW);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, unsigned long long* cellW,
+                             int Tdepth) {
+    const int threads = 256;
+    uint64_t blocks = (T + threads - 1) / threads;
+    if (blocks > 148ull * 64) blocks = 148ull * 64;
+    k_tri_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(tri, dirs, T, c->g, c->g.logN - Tdepth, cellW,
+                                                             c->d_flags);
+    c->st.launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, uint64_t* keys,
+                            uint64_t* vals, float4* ptab, uint64_t cap) {
+    const uint64_t nbatch = (T + 31) / 32;
+    uint64_t blocks = (nbatch + TRI_WARPS - 1) / TRI_WARPS;
+    if (blocks > (1ull << 30)) blocks = 1ull << 30;
+    k_tri_emit<<<(unsigned)blocks, TRI_WARPS * 32, 0, c->stream>>>(tri, dirs, T, c->g, sh, keys, vals, ptab, cap,
+                                                                   c->d_counter, c->d_flags);
+    c->st.launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace vox

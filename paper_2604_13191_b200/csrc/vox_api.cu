@@ -1,0 +1,509 @@
+// vox_api.cu -- the C ABI (include/vox.h): validation, the ctx state machine, stream-ordered
+// allocation, the per-call pipeline (bound -> plan/capacity -> emit -> sort/reduce -> merge)
+// and the multi-GPU level export/import.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "vox_internal.cuh"
+
+namespace vox {
+
+cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    return cudaMallocAsync(p, bytes, c->stream);
+}
+
+void dfree(vox_ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
+void free_level(vox_ctx* c, Level& L) {
+    dfree(c, L.key); dfree(c, L.acc); dfree(c, L.mass); dfree(c, L.m6);
+    dfree(c, L.ncl); dfree(c, L.clacc); dfree(c, L.cl);
+    L = Level();
+}
+
+void timer_begin(vox_ctx* c, StageTimer& t) {
+    if (!c->profile) return;
+    cudaEventCreate(&t.open);
+    cudaEventRecord(t.open, c->stream);
+}
+
+void timer_end(vox_ctx* c, StageTimer& t) {
+    if (!c->profile || !t.open) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, c->stream);
+    t.done.emplace_back(t.open, b);
+    t.open = nullptr;
+}
+
+static double timer_flush(StageTimer& t) {
+    for (auto& pr : t.done) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) t.ms += ms;
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    t.done.clear();
+    return t.ms;
+}
+
+}  // namespace vox
+
+using namespace vox;
+
+#define CKS(x)                                                         \
+    do {                                                               \
+        cudaError_t e_ = (x);                                          \
+        if (e_ != cudaSuccess) {                                       \
+            c->err = std::string(#x) + ": " + cudaGetErrorString(e_);  \
+            return e_ == cudaErrorMemoryAllocation ? VOX_ERR_OOM : VOX_ERR_CUDA; \
+        }                                                              \
+    } while (0)
+
+static vox_status ensure_dev(vox_ctx* c) {
+    if (c->d_flags) return VOX_OK;
+    CKS(cudaMalloc((void**)&c->d_flags, 16));
+    CKS(cudaMalloc((void**)&c->d_counter, 16));
+    upload_theta(c);
+    CKS(cudaGetLastError());
+    return VOX_OK;
+}
+
+extern "C" {
+
+const char* vox_status_str(vox_status s) {
+    switch (s) {
+        case VOX_OK: return "VOX_OK";
+        case VOX_ERR_INVALID_ARG: return "VOX_ERR_INVALID_ARG";
+        case VOX_ERR_DEGENERATE_BBOX: return "VOX_ERR_DEGENERATE_BBOX";
+        case VOX_ERR_STATE: return "VOX_ERR_STATE";
+        case VOX_ERR_OOM: return "VOX_ERR_OOM";
+        case VOX_ERR_CAPACITY: return "VOX_ERR_CAPACITY";
+        case VOX_ERR_CUDA: return "VOX_ERR_CUDA";
+        case VOX_ERR_LEVEL: return "VOX_ERR_LEVEL";
+        case VOX_ERR_COMM: return "VOX_ERR_COMM";
+    }
+    return "VOX_ERR_UNKNOWN";
+}
+
+const char* vox_last_error(vox_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], const vox_options* opt) {
+    if (!out || !bbox) return VOX_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (grid_res < 2 || grid_res > 8192 || (grid_res & (grid_res - 1))) return VOX_ERR_INVALID_ARG;
+    float e[3];
+    for (int a = 0; a < 3; a++) {
+        if (!std::isfinite(bbox[a]) || !std::isfinite(bbox[3 + a])) return VOX_ERR_DEGENERATE_BBOX;
+        e[a] = bbox[3 + a] - bbox[a];
+        if (!(e[a] > 0.0f)) return VOX_ERR_DEGENERATE_BBOX;
+    }
+    vox_options o{};
+    if (opt) o = *opt;
+    int logN = 0;
+    while ((1u << logN) < grid_res) logN++;
+    if (o.world == 0) o.world = 1;
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return VOX_ERR_INVALID_ARG;
+    if (o.top_depth == 0) o.top_depth = std::min(4, logN);
+    if (o.top_depth < 1 || o.top_depth > std::min(5, logN)) return VOX_ERR_INVALID_ARG;
+    if (o.k == 0) o.k = 3;
+    if (o.k > VOX_MAX_K) return VOX_ERR_INVALID_ARG;
+    if (o.n_slices != 0 && o.n_slices != VOX_SLICES) return VOX_ERR_INVALID_ARG;
+    vox_ctx* c = new (std::nothrow) vox_ctx();
+    if (!c) return VOX_ERR_OOM;
+    for (int a = 0; a < 3; a++) c->g.bmin[a] = bbox[a];
+    c->g.E = pmax(pmax(e[0], e[1]), e[2]);
+    c->g.N = (int)grid_res;
+    c->g.Nf = (float)grid_res;
+    c->g.logN = logN;
+    c->stream = (cudaStream_t)o.stream;
+    c->rank = o.rank;
+    c->world = o.world;
+    c->T = o.top_depth;
+    c->K = o.k;
+    c->max_bytes = o.max_bytes;
+    c->profile = o.profile;
+    c->built = 0;
+    c->st.top_depth = (uint32_t)c->T;
+    *out = c;
+    return VOX_OK;
+}
+
+static uint64_t ncells_of(const vox_ctx* c) { return 1ull << (3 * c->T); }
+
+vox_status vox_plan_shards(const uint64_t* w, uint64_t ncells, int world, uint64_t* bounds) {
+    if (!w || !bounds || world < 1 || ncells == 0) return VOX_ERR_INVALID_ARG;
+    unsigned __int128 total = 0;
+    for (uint64_t x = 0; x < ncells; x++) total += w[x];
+    bounds[0] = 0;
+    bounds[world] = ncells;
+    if (total == 0) {
+        for (int r = 1; r < world; r++) bounds[r] = (uint64_t)((unsigned __int128)ncells * r / world);
+        return VOX_OK;
+    }
+    // rank r starts at the first cell whose exclusive prefix weight reaches r/world of the total
+    unsigned __int128 pre = 0;
+    uint64_t x = 0;
+    for (int r = 1; r < world; r++) {
+        const unsigned __int128 target = total * (unsigned __int128)r;
+        while (x < ncells && pre * (unsigned __int128)world < target) pre += w[x++];
+        bounds[r] = x;
+    }
+    return VOX_OK;
+}
+
+// Common tail of the two voxelize entry points: bound (done), plan, capacity, emit, reduce.
+typedef cudaError_t (*emit_fn)(vox_ctx*, const float*, const float*, uint64_t, Shard, uint64_t*, uint64_t*,
+                               float4*, uint64_t);
+
+static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* cellW,
+                                  emit_fn emit) {
+    const uint64_t ncells = ncells_of(c);
+    std::vector<uint64_t> W(ncells);
+    unsigned fl = 0;
+    CKS(cudaMemcpyAsync(W.data(), cellW, ncells * 8, cudaMemcpyDeviceToHost, c->stream));
+    CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
+    CKS(cudaStreamSynchronize(c->stream));
+    timer_end(c, c->t_bound);
+    dfree(c, cellW);
+    if (fl) {
+        c->err = std::string("invalid input:") + ((fl & VOX_EFLAG_NONFINITE) ? " non-finite value" : "") +
+                 ((fl & VOX_EFLAG_NEG_RADIUS) ? " negative radius" : "") +
+                 ((fl & VOX_EFLAG_TOO_MANY_CAND) ? " segment with more than 2^24 candidate voxels" : "") +
+                 ((fl & VOX_EFLAG_ZERO_DIR) ? " zero-norm dir" : "");
+        return VOX_ERR_INVALID_ARG;
+    }
+    if (!c->plan_fixed) {
+        if (c->world == 1) {
+            c->cell_lo = 0;
+            c->cell_hi = ncells;
+        } else {
+            std::vector<uint64_t> bounds(c->world + 1);
+            vox_plan_shards(W.data(), ncells, c->world, bounds.data());
+            c->cell_lo = bounds[c->rank];
+            c->cell_hi = bounds[c->rank + 1];
+        }
+        c->plan_fixed = true;
+        c->st.cell_lo = c->cell_lo;
+        c->st.cell_hi = c->cell_hi;
+    }
+    uint64_t cap = 0;
+    for (uint64_t x = c->cell_lo; x < c->cell_hi; x++) cap += W[x];
+    c->st.candidates = cap;
+    c->st.pairs = 0;
+    if (cap >= (1ull << 32)) {
+        c->err = "more than 2^32 candidate voxels in one call: split the primitives into batches";
+        return VOX_ERR_CAPACITY;
+    }
+    if (cap == 0) {
+        c->state = ST_VOXELIZED;
+        return VOX_OK;
+    }
+    // estimate: pairs x2 (sort buffers) + sort temp + run scans + new leaf + ptab + merge
+    const uint64_t est = cap * 32 + cap * 16 + cap * 12 + cap * 64 + n * 16 + c->lv[0].n * 88;
+    if (c->max_bytes && est > c->max_bytes) {
+        c->err = "estimated " + std::to_string(est) + " bytes exceed max_bytes";
+        return VOX_ERR_CAPACITY;
+    }
+    uint64_t *keys = nullptr, *vals = nullptr;
+    float4* ptab = nullptr;
+    CKS(dalloc(c, (void**)&keys, cap * 16));
+    CKS(dalloc(c, (void**)&vals, cap * 16));
+    CKS(dalloc(c, (void**)&ptab, n * sizeof(float4)));
+    CKS(cudaMemsetAsync(c->d_counter, 0, 8, c->stream));
+    Shard sh;
+    sh.shift = 3 * (c->g.logN - c->T);
+    sh.cell_lo = c->cell_lo;
+    sh.cell_hi = c->cell_hi;
+    timer_begin(c, c->t_emit);
+    CKS(emit(c, a, b, n, sh, keys, vals, ptab, cap));
+    timer_end(c, c->t_emit);
+    unsigned long long P = 0;
+    CKS(cudaMemcpyAsync(&P, c->d_counter, 8, cudaMemcpyDeviceToHost, c->stream));
+    CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
+    CKS(cudaStreamSynchronize(c->stream));
+    if (fl & VOX_EFLAG_OVERFLOW) {
+        c->err = "internal: pair capacity overflow";
+        return VOX_ERR_CUDA;
+    }
+    c->st.pairs = P;
+    vox_status s = reduce_pairs(c, keys, keys + cap, vals, vals + cap, P, ptab);
+    dfree(c, keys);
+    dfree(c, vals);
+    dfree(c, ptab);
+    if (s != VOX_OK) return s;
+    c->state = ST_VOXELIZED;
+    return VOX_OK;
+}
+
+static cudaError_t emit_fibers(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh, uint64_t* keys,
+                               uint64_t* vals, float4* ptab, uint64_t cap) {
+    return launch_fiber_emit(c, seg, rad, S, sh, keys, vals, ptab, cap);
+}
+
+static cudaError_t emit_tris(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, uint64_t* keys,
+                             uint64_t* vals, float4* ptab, uint64_t cap) {
+    return launch_tri_emit(c, tri, dirs, T, sh, keys, vals, ptab, cap);
+}
+
+vox_status vox_voxelize_fibers(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (S == 0) return VOX_OK;
+    if (!segments || !radii || S >= (1ull << 32)) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    c->st.segments = S;
+    timer_begin(c, c->t_vox);
+    timer_begin(c, c->t_bound);
+    const uint64_t ncells = ncells_of(c);
+    unsigned long long* cellW = nullptr;
+    CKS(dalloc(c, (void**)&cellW, ncells * 8));
+    CKS(cudaMemsetAsync(cellW, 0, ncells * 8, c->stream));
+    CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
+    CKS(launch_fiber_bound(c, segments, radii, S, cellW, c->T));
+    s = voxelize_common(c, segments, radii, S, cellW, emit_fibers);
+    timer_end(c, c->t_vox);
+    return s;
+}
+
+vox_status vox_voxelize_triangles(vox_ctx* c, const float* tris, const float* dirs, uint64_t T) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (T == 0) return VOX_OK;
+    if (!tris || T >= (1ull << 32)) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    c->st.segments = T;
+    timer_begin(c, c->t_vox);
+    timer_begin(c, c->t_bound);
+    const uint64_t ncells = ncells_of(c);
+    unsigned long long* cellW = nullptr;
+    CKS(dalloc(c, (void**)&cellW, ncells * 8));
+    CKS(cudaMemsetAsync(cellW, 0, ncells * 8, c->stream));
+    CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
+    CKS(launch_tri_bound(c, tris, dirs, T, cellW, c->T));
+    s = voxelize_common(c, tris, dirs, T, cellW, emit_tris);
+    timer_end(c, c->t_vox);
+    return s;
+}
+
+vox_status vox_voxelize_fibers_host(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (S == 0) return VOX_OK;
+    if (!segments || !radii) return VOX_ERR_INVALID_ARG;
+    float *ds = nullptr, *dr = nullptr;
+    CKS(dalloc(c, (void**)&ds, S * 24));
+    CKS(dalloc(c, (void**)&dr, S * 4));
+    CKS(cudaMemcpyAsync(ds, segments, S * 24, cudaMemcpyHostToDevice, c->stream));
+    CKS(cudaMemcpyAsync(dr, radii, S * 4, cudaMemcpyHostToDevice, c->stream));
+    vox_status s = vox_voxelize_fibers(c, ds, dr, S);
+    dfree(c, ds);
+    dfree(c, dr);
+    return s;
+}
+
+vox_status vox_voxelize_triangles_host(vox_ctx* c, const float* tris, const float* dirs, uint64_t T) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (T == 0) return VOX_OK;
+    if (!tris) return VOX_ERR_INVALID_ARG;
+    float *dt = nullptr, *dd = nullptr;
+    CKS(dalloc(c, (void**)&dt, T * 36));
+    CKS(cudaMemcpyAsync(dt, tris, T * 36, cudaMemcpyHostToDevice, c->stream));
+    if (dirs) {
+        CKS(dalloc(c, (void**)&dd, T * 12));
+        CKS(cudaMemcpyAsync(dd, dirs, T * 12, cudaMemcpyHostToDevice, c->stream));
+    }
+    vox_status s = vox_voxelize_triangles(c, dt, dd, T);
+    dfree(c, dt);
+    dfree(c, dd);
+    return s;
+}
+
+vox_status vox_build_lod(vox_ctx* c, uint32_t levels) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if ((int)levels > c->g.logN) return VOX_ERR_LEVEL;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    int limit = (int)levels;
+    const int Lt = c->g.logN - c->T;
+    if (c->world > 1 && c->imported_level < 0 && limit > Lt) limit = Lt;
+    timer_begin(c, c->t_lodall);
+    for (int l = c->built + 1; l <= limit; l++) {
+        s = build_level(c, l);
+        if (s != VOX_OK) return s;
+        c->built = l;
+    }
+    timer_end(c, c->t_lodall);
+    c->state = ST_LOD;
+    return VOX_OK;
+}
+
+vox_status vox_built_levels(vox_ctx* c, uint32_t* out) {
+    if (!c || !out) return VOX_ERR_INVALID_ARG;
+    *out = (uint32_t)c->built;
+    return VOX_OK;
+}
+
+vox_status vox_read_level(vox_ctx* c, uint32_t level, vox_level_view* out) {
+    if (!c || !out) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    const Level& L = c->lv[level];
+    out->n = L.n;
+    out->key = L.key;
+    out->mass = L.mass;
+    out->m6 = L.m6;
+    out->acc = reinterpret_cast<const int64_t*>(L.acc);
+    out->ncl = level == 0 ? nullptr : L.ncl;
+    out->cl = level == 0 ? nullptr : L.cl;
+    return VOX_OK;
+}
+
+__global__ void k_leaf_lobes(uint64_t n, const float* __restrict__ mass, const float* __restrict__ m6, int K,
+                             uint8_t* __restrict__ ncl, float* __restrict__ cl) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const bool has = mass[v] > 0.0f;
+        if (ncl) ncl[v] = has ? 1 : 0;
+        if (cl) {
+            for (int q = 0; q < K; q++)
+                for (int e = 0; e < 7; e++)
+                    cl[(v * K + q) * 7 + e] = (q == 0 && has) ? (e == 0 ? mass[v] : m6[6 * v + e - 1]) : 0.0f;
+        }
+    }
+}
+
+vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass, float* m6, uint8_t* ncl, float* cl) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    const Level& L = c->lv[level];
+    const uint64_t n = L.n;
+    const uint32_t K = c->K;
+    if (n == 0) return VOX_OK;
+    if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, c->stream));
+    if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, c->stream));
+    if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, c->stream));
+    if (level > 0) {
+        if (ncl) CKS(cudaMemcpyAsync(ncl, L.ncl, n, cudaMemcpyDefault, c->stream));
+        if (cl) CKS(cudaMemcpyAsync(cl, L.cl, n * K * 28, cudaMemcpyDefault, c->stream));
+    } else if (ncl || cl) {
+        uint8_t* dn = nullptr;
+        float* dc = nullptr;
+        if (ncl) CKS(dalloc(c, (void**)&dn, n));
+        if (cl) CKS(dalloc(c, (void**)&dc, n * K * 28));
+        uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 32);
+        k_leaf_lobes<<<(unsigned)blocks, 256, 0, c->stream>>>(n, L.mass, L.m6, (int)K, dn, dc);
+        c->st.launches++;
+        if (ncl) CKS(cudaMemcpyAsync(ncl, dn, n, cudaMemcpyDefault, c->stream));
+        if (cl) CKS(cudaMemcpyAsync(cl, dc, n * K * 28, cudaMemcpyDefault, c->stream));
+        dfree(c, dn);
+        dfree(c, dc);
+    }
+    CKS(cudaStreamSynchronize(c->stream));
+    return VOX_OK;
+}
+
+vox_status vox_copy_level_acc(vox_ctx* c, uint32_t level, int64_t* acc) {
+    if (!c || !acc) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    const Level& L = c->lv[level];
+    if (L.n == 0) return VOX_OK;
+    CKS(cudaMemcpyAsync(acc, L.acc, L.n * 56, cudaMemcpyDefault, c->stream));
+    CKS(cudaStreamSynchronize(c->stream));
+    return VOX_OK;
+}
+
+vox_status vox_export_level(vox_ctx* c, uint32_t level, void* buf, uint64_t* bytes) {
+    if (!c || !bytes) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    const uint64_t need = c->lv[level].n * record_bytes(c->K);
+    if (!buf) {
+        *bytes = need;
+        return VOX_OK;
+    }
+    if (*bytes < need) return VOX_ERR_COMM;
+    CKS(launch_pack(c, (int)level, buf));
+    *bytes = need;
+    return VOX_OK;
+}
+
+vox_status vox_import_level(vox_ctx* c, uint32_t level, const void* buf, uint64_t bytes) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->g.logN) return VOX_ERR_LEVEL;
+    const uint64_t rb = record_bytes(c->K);
+    if (bytes % rb != 0 || (bytes && !buf)) return VOX_ERR_COMM;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    for (int l = (int)level + 1; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
+    s = unpack_level(c, (int)level, buf, bytes / rb);
+    if (s != VOX_OK) return s;
+    c->imported_level = (int)level;
+    c->built = (int)level;
+    if (c->state == ST_CREATED) c->state = ST_VOXELIZED;
+    return VOX_OK;
+}
+
+vox_status vox_theta_table(float* theta, float* coef) {
+    if (!theta || !coef) return VOX_ERR_INVALID_ARG;
+    float t[32][3], k[32][6];
+    host_theta(t, k);
+    std::memcpy(theta, t, sizeof(t));
+    std::memcpy(coef, k, sizeof(k));
+    return VOX_OK;
+}
+
+vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
+    if (!c || !out) return VOX_ERR_INVALID_ARG;
+    CKS(cudaStreamSynchronize(c->stream));
+    c->st.ms_bound = timer_flush(c->t_bound);
+    c->st.ms_emit = timer_flush(c->t_emit);
+    c->st.ms_sort = timer_flush(c->t_sort);
+    c->st.ms_reduce = timer_flush(c->t_reduce);
+    c->st.ms_merge = timer_flush(c->t_merge);
+    c->st.ms_lod_scan = timer_flush(c->t_lodscan);
+    c->st.ms_lod = timer_flush(c->t_lod);
+    c->st.ms_total_vox = timer_flush(c->t_vox);
+    c->st.ms_total_lod = timer_flush(c->t_lodall);
+    *out = c->st;
+    return VOX_OK;
+}
+
+vox_status vox_stats_reset(vox_ctx* c) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    vox_stats tmp;
+    vox_stats_get(c, &tmp);
+    for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
+                          &c->t_vox, &c->t_lodall})
+        t->ms = 0.0;
+    c->st.launches = 0;
+    return VOX_OK;
+}
+
+vox_status vox_sync(vox_ctx* c) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    CKS(cudaStreamSynchronize(c->stream));
+    return VOX_OK;
+}
+
+void vox_destroy(vox_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
+    for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
+                          &c->t_vox, &c->t_lodall}) {
+        timer_flush(*t);
+        if (t->open) cudaEventDestroy(t->open);
+    }
+    cudaStreamSynchronize(c->stream);
+    if (c->d_flags) cudaFree(c->d_flags);
+    if (c->d_counter) cudaFree(c->d_counter);
+    delete c;
+}
+
+}  // extern "C"

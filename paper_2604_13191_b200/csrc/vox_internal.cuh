@@ -1,0 +1,167 @@
+// vox_internal.cuh -- internal declarations of libvox (product path; shares nothing with oracle/).
+//
+// All floating-point code in this library is compiled with -fmad=false, -prec-div=true,
+// -prec-sqrt=true and without fast-math, so every expression below is the pinned
+// sequence of IEEE binary32 operations of docs/PREDICATES.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vox.h"
+
+#define VOX_MAX_LEVELS 14
+#define VOX_MAX_K 8
+#define VOX_SLICES 32
+
+// device error flags (bitmask)
+#define VOX_EFLAG_NONFINITE 1u
+#define VOX_EFLAG_NEG_RADIUS 2u
+#define VOX_EFLAG_TOO_MANY_CAND 4u
+#define VOX_EFLAG_ZERO_DIR 8u
+#define VOX_EFLAG_OVERFLOW 16u
+
+namespace vox {
+
+// ---------------------------------------------------------------- pinned helpers (PREDICATES)
+
+__host__ __device__ __forceinline__ float pmin(float a, float b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ float pmax(float a, float b) { return a > b ? a : b; }
+
+// §8 fixed point: q(x) = round-to-nearest-even(x * 2^32)
+__device__ __forceinline__ long long q32(float x) { return __float2ll_rn(x * 4294967296.0f); }
+__device__ __forceinline__ float deq32(long long a) { return __ll2float_rn(a) * 2.3283064365386963e-10f; }
+
+// §2 Morton encoding (x in bit 0) by bit spreading
+__host__ __device__ __forceinline__ uint64_t spread3(uint32_t v) {
+    uint64_t x = v & 0x1fffffu;
+    x = (x | (x << 32)) & 0x1f00000000ffffull;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+    x = (x | (x << 8)) & 0x100f00f00f00f00full;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+__host__ __device__ __forceinline__ uint64_t morton3(uint32_t i, uint32_t j, uint32_t k) {
+    return spread3(i) | (spread3(j) << 1) | (spread3(k) << 2);
+}
+__host__ __device__ __forceinline__ uint32_t compact3(uint64_t x) {
+    x &= 0x1249249249249249ull;
+    x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+    x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+    x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+    x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+    x = (x ^ (x >> 32)) & 0x1fffffull;
+    return (uint32_t)x;
+}
+
+// §1 grid transform
+struct GridXf {
+    float bmin[3];
+    float E;
+    float Nf;
+    int N;
+    int logN;
+};
+
+__device__ __forceinline__ float to_grid(const GridXf& g, int a, float p) {
+    float t = p - g.bmin[a];
+    t = t / g.E;
+    return t * g.Nf;
+}
+__device__ __forceinline__ float to_grid_len(const GridXf& g, float r) {
+    float t = r / g.E;
+    return t * g.Nf;
+}
+
+// Shard filter: keys whose top cell (key >> shift) lies in [lo, hi) are emitted.
+struct Shard {
+    int shift;          // 3 * (logN - T)
+    uint64_t cell_lo, cell_hi;
+};
+
+// ---------------------------------------------------------------- host-side state
+
+struct Level {
+    uint64_t n = 0;
+    uint64_t* key = nullptr;
+    long long* acc = nullptr;   // [n][7]
+    float* mass = nullptr;      // [n]
+    float* m6 = nullptr;        // [n][6]
+    uint8_t* ncl = nullptr;     // [n]       (levels >= 1)
+    long long* clacc = nullptr; // [n][K][7] (levels >= 1)
+    float* cl = nullptr;        // [n][K][7] (levels >= 1)
+};
+
+enum CtxState { ST_CREATED = 0, ST_VOXELIZED = 1, ST_LOD = 2 };
+
+// Per-stage CUDA-event timing without host syncs: begin/end events are recorded on the ctx
+// stream and resolved in vox_stats_get.
+struct StageTimer {
+    cudaEvent_t open = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> done;
+    double ms = 0.0;
+};
+
+}  // namespace vox
+
+struct vox_ctx {
+    vox::GridXf g;
+    cudaStream_t stream = nullptr;
+    int rank = 0, world = 1, T = 0;
+    uint32_t K = 3;
+    uint64_t max_bytes = 0;
+    int profile = 0;
+    int state = vox::ST_CREATED;
+    int built = 0;
+    int imported_level = -1;
+    bool plan_fixed = false;
+    uint64_t cell_lo = 0, cell_hi = 0;
+    vox::Level lv[VOX_MAX_LEVELS];
+    unsigned int* d_flags = nullptr;        // device error flags
+    unsigned long long* d_counter = nullptr; // pair cursor
+    vox_stats st{};
+    std::string err;
+    // stage timers (profile = 1)
+    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall;
+};
+
+namespace vox {
+
+// allocation helpers (stream-ordered)
+cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes);
+void dfree(vox_ctx* c, void* p);
+void free_level(vox_ctx* c, Level& L);
+void timer_begin(vox_ctx* c, StageTimer& t);
+void timer_end(vox_ctx* c, StageTimer& t);
+
+// ---------------------------------------------------------------- kernel launchers
+
+// fibers (k_fiber.cu)
+cudaError_t launch_fiber_bound(vox_ctx* c, const float* seg, const float* rad, uint64_t S,
+                               unsigned long long* cellW, int T);
+cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh,
+                              uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap);
+// triangles (k_tri.cu)
+cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, unsigned long long* cellW,
+                             int Tdepth);
+cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh,
+                            uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap);
+// sort + segmented reduce (k_reduce.cu): pairs -> new leaf set merged into lv[0]
+vox_status reduce_pairs(vox_ctx* c, uint64_t* keys, uint64_t* keys_alt, uint64_t* vals, uint64_t* vals_alt,
+                        uint64_t P, const float4* ptab);
+// LoD (k_lod.cu)
+vox_status build_level(vox_ctx* c, int l);
+void upload_theta(vox_ctx* c);
+void host_theta(float theta[32][3], float coef[32][6]);
+// fp32 outputs of a level from its accumulators (k_lod.cu)
+cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters);
+// multi-GPU records (k_lod.cu)
+uint64_t record_bytes(uint32_t K);
+cudaError_t launch_pack(vox_ctx* c, int level, void* buf);
+vox_status unpack_level(vox_ctx* c, int level, const void* buf, uint64_t n);
+
+}  // namespace vox

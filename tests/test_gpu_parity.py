@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Key sets bit-exact; mass/M and every lobe bit-exact by construction (PREDICATES §8), which
+implies north_star's 1e-5 relative tolerance (asserted separately on the fp32 outputs)."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2604_13191_b200 import build
+    build.build()
+    import paper_2604_13191_b200 as P
+    return P
+
+
+def _cmp_level(g, r, l, tag=""):
+    gk = g["key"].cpu().numpy().astype(np.uint64)
+    assert gk.shape == r["key"].shape, f"{tag} level {l}: {gk.shape} vs {r['key'].shape} voxels"
+    assert np.array_equal(gk, r["key"]), f"{tag} level {l} keys"
+    assert np.array_equal(g["acc"].cpu().numpy(), r["acc"]), f"{tag} level {l} accumulators"
+    gm, rm = g["mass"].cpu().numpy(), r["mass"]
+    assert np.allclose(gm, rm, rtol=1e-5, atol=0), f"{tag} level {l} mass (1e-5)"
+    assert np.array_equal(gm, rm) and np.array_equal(g["m6"].cpu().numpy(), r["m6"])
+    if l > 0:
+        assert np.array_equal(g["ncl"].cpu().numpy(), r["ncl"]), f"{tag} level {l} ncl"
+        assert np.array_equal(g["cl"].cpu().numpy(), r["cl"]), f"{tag} level {l} lobes"
+
+
+def _run_both(P, N, bbox, levels, segs=None, radii=None, tris=None, dirs=None, k=3, parts=1):
+    v = P.Vox(N, bbox, k=k)
+    o = oracle.Oracle(N, np.asarray(bbox, np.float32), k)
+    if segs is not None:
+        for idx in np.array_split(np.arange(len(segs)), parts):
+            v.voxelize_fibers(torch.from_numpy(np.ascontiguousarray(segs[idx])).cuda(),
+                              torch.from_numpy(np.ascontiguousarray(radii[idx])).cuda())
+        o.add_fibers(segs, radii)
+    if tris is not None:
+        v.voxelize_triangles(torch.from_numpy(tris).cuda(), None if dirs is None else torch.from_numpy(dirs).cuda())
+        o.add_triangles(tris, dirs)
+    v.build_lod(levels)
+    o.build(levels)
+    return v, o
+
+
+def test_config1_icosphere_all_levels(P):
+    c = gen.config(1)
+    v, o = _run_both(P, c["grid_res"], c["bbox"], c["levels"], tris=c["tris"])
+    for l in range(c["levels"] + 1):
+        _cmp_level(v.level(l), o.level(l), l, "icosphere")
+
+
+def test_config2_plain_weave_all_levels(P):
+    c = gen.config(2)
+    v, o = _run_both(P, c["grid_res"], c["bbox"], c["levels"], segs=c["segments"], radii=c["radii"])
+    for l in range(c["levels"] + 1):
+        _cmp_level(v.level(l), o.level(l), l, "weave")
+    st = v.stats()
+    assert st["pairs"] <= st["candidates"]
+
+
+@pytest.mark.parametrize("seed,n,N,rscale", [(0, 1, 32, 1.0), (1, 37, 64, 0.3), (2, 1000, 64, 1.0),
+                                               (3, 4099, 128, 2.0), (4, 20000, 256, 0.7)])
+def test_random_fibers_ragged(P, seed, n, N, rscale):
+    """Random segments incl. ones straddling or outside the bbox, zero-length and r = 0."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(-0.1, 1.1, (n, 3))
+    b = a + rng.normal(0, 3.0 / N, (n, 3))
+    segs = np.stack([a, b], 1).astype(np.float32)
+    radii = (rng.uniform(0.0, 1.5, n) * rscale / N).astype(np.float32)
+    if n > 10:
+        segs[3, 1] = segs[3, 0]        # zero-length (sphere)
+        radii[5] = 0.0                 # r = 0 (zero-volume fiber)
+    L = int(np.log2(N))
+    v, o = _run_both(P, N, [0, 0, 0, 1, 1, 1], L, segs=segs, radii=radii)
+    for l in range(L + 1):
+        _cmp_level(v.level(l), o.level(l), l, f"fibers{seed}")
+
+
+def test_triangles_tangent_mode_and_k(P):
+    t, d = gen.ridge_mesh(n_quads=40, ridges=10, height=4 / 256, noise_amp=0.5 / 256)
+    for k in (1, 2, 3, 8):
+        v, o = _run_both(P, 256, [0, 0, 0, 1, 1, 1], 8, tris=t, dirs=d, k=k)
+        for l in range(9):
+            _cmp_level(v.level(l), o.level(l), l, f"ridge k={k}")
+
+
+def test_mixed_and_split_calls(P):
+    s, r = gen.plain_weave(n_warp=16, n_weft=16, n_seg=32, pitch=1 / 16)
+    tris = gen.icosphere(2, radius=0.3)
+    v = P.Vox(128, [0, 0, 0, 1, 1, 1])
+    o = oracle.Oracle(128, np.array([0, 0, 0, 1, 1, 1], np.float32))
+    perm = np.random.default_rng(1).permutation(len(s))
+    for idx in np.array_split(perm, 3):
+        v.voxelize_fibers(torch.from_numpy(s[idx]).cuda(), torch.from_numpy(r[idx]).cuda())
+    v.voxelize_triangles(torch.from_numpy(tris).cuda())
+    o.add_fibers(s, r)
+    o.add_triangles(tris)
+    v.build_lod(7)
+    o.build(7)
+    for l in range(8):
+        _cmp_level(v.level(l), o.level(l), l, "mixed")
+
+
+def test_host_entry_points(P):
+    c = gen.config(1)
+    v = P.Vox(c["grid_res"], c["bbox"])
+    v.voxelize_triangles_host(c["tris"])
+    v.build_lod(6)
+    o = oracle.Oracle(c["grid_res"], c["bbox"])
+    o.add_triangles(c["tris"])
+    o.build(6)
+    for l in range(7):
+        _cmp_level(v.level(l, device="cpu"), o.level(l), l, "host")
+
+
+def test_errors_and_states(P):
+    v = P.Vox(64, [0, 0, 0, 1, 1, 1])
+    bad = torch.tensor([[[0.1, 0.1, 0.1], [0.2, float("nan"), 0.2]]], device="cuda")
+    with pytest.raises(P.VoxError) as e:
+        v.voxelize_fibers(bad, torch.tensor([0.01], device="cuda"))
+    assert e.value.name == "VOX_ERR_INVALID_ARG"
+    ok = torch.tensor([[[0.1, 0.1, 0.1], [0.2, 0.2, 0.2]]], device="cuda")
+    with pytest.raises(P.VoxError):
+        v.voxelize_fibers(ok, torch.tensor([-0.01], device="cuda"))
+    with pytest.raises(P.VoxError):
+        v.voxelize_triangles(torch.rand(2, 3, 3, device="cuda"), torch.zeros(2, 3, device="cuda"))
+    assert v.level(0)["key"].numel() == 0                      # unchanged after errors
+    v.voxelize_fibers(torch.zeros(0, 2, 3, device="cuda"), torch.zeros(0, device="cuda"))   # S = 0 no-op
+    with pytest.raises(P.VoxError) as e:
+        v.level(1)
+    assert e.value.name == "VOX_ERR_LEVEL"
+    with pytest.raises(P.VoxError) as e:
+        v.build_lod(7)
+    assert e.value.name == "VOX_ERR_LEVEL"
+    v.voxelize_fibers(ok, torch.tensor([0.01], device="cuda"))
+    v.build_lod(6)
+    with pytest.raises(P.VoxError) as e:
+        v.voxelize_fibers(ok, torch.tensor([0.01], device="cuda"))
+    assert e.value.name == "VOX_ERR_STATE"
+    # capacity cap refuses before allocating
+    w = P.Vox(64, [0, 0, 0, 1, 1, 1], max_bytes=1000)
+    with pytest.raises(P.VoxError) as e:
+        w.voxelize_fibers(ok, torch.tensor([0.05], device="cuda"))
+    assert e.value.name == "VOX_ERR_CAPACITY"
+
+
+def test_fake_world_sharding_equals_unsharded(P):
+    """T4 fake world: R Morton shards run one after another on one GPU; the
+    union of their local levels and the gathered top levels equal the unsharded result."""
+    s, r = gen.plain_weave(n_warp=32, n_weft=32, n_seg=64, pitch=1 / 32)
+    S, R = torch.from_numpy(s).cuda(), torch.from_numpy(r).cuda()
+    N, L = 256, 8
+    full = P.Vox(N, [0, 0, 0, 1, 1, 1])
+    full.voxelize_fibers(S, R)
+    full.build_lod(L)
+    for world in (2, 3, 8):
+        shards = [P.Vox(N, [0, 0, 0, 1, 1, 1], rank=q, world=world) for q in range(world)]
+        for v in shards:
+            v.voxelize_fibers(S, R)
+            v.build_lod(L)                      # stops at log2(N) - T without the gather
+        T = shards[0].stats()["top_depth"]
+        lt = L - T
+        assert all(v.built_levels() == lt for v in shards)
+        for l in range(lt + 1):
+            got = [v.level(l) for v in shards]
+            ref = full.level(l)
+            for key in ("key", "acc", "mass", "m6", "ncl", "cl"):
+                assert torch.equal(torch.cat([g[key] for g in got]), ref[key]), (world, l, key)
+        recs = torch.cat([v.export_level(lt) for v in shards])   # = the all-gather, in rank order
+        for v in shards:
+            v.import_level(lt, recs)
+            v.build_lod(L)
+            for l in range(lt, L + 1):
+                g, ref = v.level(l), full.level(l)
+                for key in ("key", "acc", "ncl", "cl"):
+                    assert torch.equal(g[key], ref[key]), (world, l, key)
+
+
+def test_deterministic_repeat(P):
+    c = gen.config(2)
+    outs = []
+    for _ in range(2):
+        v = P.Vox(c["grid_res"], c["bbox"])
+        v.voxelize_fibers(torch.from_numpy(c["segments"]).cuda(), torch.from_numpy(c["radii"]).cuda())
+        v.build_lod(9)
+        outs.append([v.level(l) for l in range(10)])
+    for a, b in zip(*outs):
+        for k in a:
+            assert torch.equal(a[k], b[k])
