@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: voxelize + full LoD build (one "step") on the BASELINE.json
+workload, printed as ONE JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1: Morton-range shards)
+
+Workload (default): config 4 -- explicit-fiber knit, ~10M segments at 4096^3, 12 levels
+(synthetic, seeded; gen.knit). Inputs are resident in HBM before the timed region; they are
+larger than L2 (280 MB > 126 MB), so no L2 flush is needed between steps.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on bounded samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fiber segments voxelized/s + full LoD build ms; achieved HBM GB/s vs 8 TB/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi SM clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._p = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self._p:
+            time.sleep(0.25)
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=2)
+            except Exception:
+                self._p.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def _workload(cfg: int, n_segments: int | None):
+    import gen
+    kw = {}
+    if n_segments:
+        kw["n_segments"] = n_segments
+    c = gen.config(cfg, **kw)
+    return c
+
+
+def _cell_sample(seg, bbox, N, level, target):
+    """Pick the Morton cell at `level` whose segment count is closest to `target`
+    (a bounded, spatially complete sample for the oracle). Returns (cell, count)."""
+    E = float(np.max(bbox[3:] - bbox[:3]))
+    mid = 0.5 * (seg[:, 0].astype(np.float64) + seg[:, 1])
+    g = np.floor((mid - bbox[:3]) / E * N).astype(np.int64) >> level
+    g = np.clip(g, 0, (N >> level) - 1)
+    cells = np.zeros(len(g), np.uint64)
+    for b in range(12):
+        for a in range(3):
+            cells |= ((g[:, a].astype(np.uint64) >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+    u, cnt = np.unique(cells, return_counts=True)
+    i = int(np.argmin(np.abs(cnt - target)))
+    return int(u[i]), int(cnt[i])
+
+
+def oracle_sample(c, target_segments: int, level: int):
+    """Time the oracle (single-threaded, as it stands) on one Morton-cell window: every
+    segment touching the cell is voxelized (its S_p needs all its keys) and the LoD is built
+    inside the window up to `level`. Returns (segments processed, seconds, description)."""
+    import oracle
+    seg, rad, bbox, N = c["segments"], c["radii"], c["bbox"], c["grid_res"]
+    cell, _ = _cell_sample(seg, bbox, N, level, target_segments)
+    # segments whose candidate box can touch the window (cheap host prefilter, the oracle
+    # culls exactly)
+    E = float(np.max(bbox[3:] - bbox[:3]))
+    lo = np.minimum(seg[:, 0], seg[:, 1]) - rad[:, None]
+    hi = np.maximum(seg[:, 0], seg[:, 1]) + rad[:, None]
+    gi = [0, 0, 0]
+    import oracle as O
+    i, j, k = O.unmorton(cell)
+    box_lo = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
+    box_hi = box_lo + ((1 << level) + 4) * E / N
+    sel = np.all((hi >= box_lo) & (lo <= box_hi), axis=1)
+    s, r = np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
+    o = oracle.Oracle(N, bbox)
+    o.set_window(level, cell)
+    t0 = time.perf_counter()
+    o.add_fibers(s, r)
+    o.build(level)
+    dt = time.perf_counter() - t0
+    desc = (f"oracle (plain C, 1 thread) on Morton cell {cell} at level {level} "
+            f"({(1 << level)}^3 voxels): {len(s)} segments touching it voxelized + LoD levels 1..{level} inside it")
+    del gi
+    return len(s), dt, desc
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, bounded samples."""
+    c = _workload(args.config, args.segments)
+    lvl = 7 if c["grid_res"] >= 2048 else max(1, int(math.log2(c["grid_res"])) - 2)
+    times, counts, desc = [], [], ""
+    for it in range(args.warmup + args.steps):
+        n, dt, desc = oracle_sample(c, args.ref_segments, lvl)
+        if it >= args.warmup:
+            times.append(dt)
+            counts.append(n)
+    value = sum(counts) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "segments/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"config {args.config} sample: {desc}"},
+            "cpu_baseline": {"value": value, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "segments/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--segments", type=int, default=None, help="override the segment count (quick runs)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-segments", type=int, default=150_000, help="oracle sample size (cpu_baseline)")
+    ap.add_argument("--ref-segments", type=int, default=40_000, help="oracle sample size per reference step")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_13191_b200 import Vox, build as vbuild
+    vbuild.build()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = _workload(args.config, args.segments)
+    N, levels, bbox = c["grid_res"], c["levels"], c["bbox"]
+    fib = c["kind"] == "fiber"
+    if fib:
+        h_a, h_b = c["segments"], c["radii"]
+    else:
+        h_a, h_b = c["tris"], c["dirs"]
+    n_prims = len(h_a)
+    d_a = torch.from_numpy(h_a).cuda()
+    d_b = torch.from_numpy(h_b).cuda() if h_b is not None else None
+    stream = torch.cuda.current_stream()
+
+    def step(profile=False):
+        v = Vox(N, bbox, rank=rank, world=world, profile=profile)
+        if fib:
+            v.voxelize_fibers(d_a, d_b)
+        else:
+            v.voxelize_triangles(d_a, d_b)
+        v.build_lod(levels, group)
+        return v
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step().close()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    # ---------------------------------------------------------------- timed region (device time)
+    stage = {}
+    counts = {}
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            v = step(profile=True)
+            st = v.stats()
+            for k2 in ("ms_bound", "ms_emit", "ms_sort", "ms_reduce", "ms_merge", "ms_lod_scan", "ms_lod",
+                       "ms_total_vox", "ms_total_lod"):
+                stage[k2] = stage.get(k2, 0.0) + st[k2]
+            launches += st["launches"]
+            counts = {"pairs": st["pairs"], "candidates": st["candidates"], "voxels": st["voxels"]}
+            if not counts.get("levels"):
+                counts["levels"] = [int(v.view(l)["n"]) for l in range(levels + 1)]
+            v.close()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n_prims * args.steps / (ms / 1e3)
+    for k2 in stage:
+        stage[k2] /= args.steps
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    V = counts["levels"]
+    P = counts["pairs"]
+    bytes_vox = 28 * n_prims + 32 * P + 36 * V[0]
+    bytes_lod = sum((36 * V[0] if l == 1 else 121 * V[l - 1]) + 121 * V[l] for l in range(1, levels + 1))
+    kernels = {
+        "k_fiber_emit" if fib else "k_tri_emit": stage["ms_emit"],
+        "radix_sort(pairs)": stage["ms_sort"],
+        "k_segreduce": stage["ms_reduce"],
+        "k_pyramid(sggxh)": stage["ms_lod"],
+    }
+    dom = max(kernels, key=kernels.get)
+    alg = {"k_fiber_emit": 28 * n_prims + 16 * P + 16 * n_prims, "k_tri_emit": 36 * n_prims + 16 * P + 16 * n_prims,
+           "radix_sort(pairs)": 32 * P, "k_segreduce": 16 * P + 16 * n_prims + 64 * V[0],
+           "k_pyramid(sggxh)": bytes_lod}[dom]
+    dur = kernels[dom] / 1e3
+    roof = {"kernel": dom, "bound": "hbm", "achieved": alg / dur / 1e9 if dur > 0 else None, "peak": hbm,
+            "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "when" in peaks else "fallback",
+            "traffic": None, "alg_bytes_per_launch": alg, "ms_per_launch": kernels[dom]}
+    roof["frac"] = roof["achieved"] / hbm if roof["achieved"] else None
+
+    line = {"metric": METRIC, "value": value, "unit": "segments/s" if fib else "triangles/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config],
+                       "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
+                       "l2": "inputs (28 B x prims) larger than L2; no flush"},
+            "lod_ms": stage["ms_total_lod"], "vox_ms": stage["ms_total_vox"],
+            "hbm_alg_gbs_full_build": (bytes_vox + bytes_lod) / (ms_step / 1e3) / 1e9,
+            "stages_ms": {k2: round(v2, 4) for k2, v2 in stage.items()},
+            "counts": {"pairs": P, "candidates": counts["candidates"], "voxels_per_level": V},
+            "roofline": roof, "gpu_launches": launches}
+
+    # ---------------------------------------------------------------- e2e through the C ABI, host buffers
+    if not args.no_e2e:
+        pa = torch.from_numpy(h_a).pin_memory()
+        pb = torch.from_numpy(h_b).pin_memory() if h_b is not None else None
+        outs = {}
+
+        def e2e_step():
+            v = Vox(N, bbox, rank=rank, world=world)
+            if fib:
+                v.voxelize_fibers_host(pa, pb)
+            else:
+                v.voxelize_triangles_host(pa, pb)
+            v.build_lod(levels, group)
+            d2h = 0
+            for l in range(1, levels + 1):   # the LoD volumes delivered to the host (levels 1..L)
+                lv = v.level(l, device="cpu")
+                d2h += sum(t.numel() * t.element_size() for k3, t in lv.items() if k3 != "acc")
+            v.close()
+            outs["d2h"] = d2h
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        line["e2e"] = {"value": n_prims * args.steps / (ems / 1e3), "unit": line["unit"],
+                       "h2d_bytes_per_step": int(h_a.nbytes + (h_b.nbytes if h_b is not None else 0)),
+                       "d2h_bytes_per_step": int(outs["d2h"]),
+                       "wall_s": time.perf_counter() - t0}
+    line["clocks"] = clk.summary()
+
+    # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and fib:
+        lvl = 7 if N >= 2048 else max(1, int(math.log2(N)) - 2)
+        n, dt, desc = oracle_sample(c, args.cpu_segments, lvl)
+        line["cpu_baseline"] = {"value": n / dt, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc,
+                                "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

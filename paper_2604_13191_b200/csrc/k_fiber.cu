@@ -171,6 +171,25 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
     return true;
 }
 
+// GPU-only conservative early reject (not part of the pinned definition): the voxel cannot be
+// a key when its centre is farther than r + sqrt(3)/2 + 0.05 voxel from the segment, because
+// every point of the box lies within sqrt(3)/2 of the centre and the pinned fp32 predicate
+// deviates from the exact one by orders of magnitude less than 0.05 voxel. Parity tests
+// compare the emitted key sets with the oracle, which has no such shortcut.
+__device__ __forceinline__ bool far_from_capsule(const Fib& f, const float* d, float rg, int64_t i, int64_t j,
+                                                 int64_t k) {
+    const float e0 = ((float)i + 0.5f) - f.a[0], e1 = ((float)j + 0.5f) - f.a[1], e2 = ((float)k + 0.5f) - f.a[2];
+    const float ww = f.w[0] + f.w[1] + f.w[2];
+    float t = 0.0f;
+    if (ww > 0.0f) {
+        t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) / ww;
+        t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
+    }
+    const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
+    const float thr = rg + 0.91602540378f;   // sqrt(3)/2 + 0.05
+    return q0 * q0 + q1 * q1 + q2 * q2 > thr * thr;
+}
+
 // ---------------------------------------------------------------- emit
 
 constexpr int EMIT_WARPS = 8;
@@ -180,11 +199,11 @@ constexpr int EMIT_WARPS = 8;
 // lane evaluates one (segment, voxel) candidate per step whatever the segment sizes.
 // Keys add q(l_r) into the segment's exact S_acc (shared int64); in-grid, in-shard keys are
 // compacted with a warp ballot and appended to the pair stream with one atomic per warp step.
-__global__ void __launch_bounds__(EMIT_WARPS * 32)
+__global__ void __launch_bounds__(EMIT_WARPS * 32, 3)
 k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g, Shard sh,
              uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab, uint64_t cap,
              unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
-    __shared__ float s_f[EMIT_WARPS][12][32];
+    __shared__ float s_f[EMIT_WARPS][16][32];
     __shared__ int64_t s_u0[EMIT_WARPS][3][32];
     __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
     __shared__ uint32_t s_start[EMIT_WARPS][32];
@@ -231,6 +250,8 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             s_f[wib][9][lane] = f.r2;
             s_f[wib][10][lane] = __uint_as_float(f.moving);
             s_f[wib][11][lane] = f.len;
+            for (int ax = 0; ax < 3; ax++) s_f[wib][12 + ax][lane] = d[ax];
+            s_f[wib][15][lane] = rg;
         }
         // warp inclusive scan of the candidate counts
         uint32_t incl = cnt;
@@ -246,8 +267,10 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             const uint32_t c = c0 + lane;
             bool emit = false;
             uint64_t mkey = 0, val = 0;
+            long long qv = 0;
+            int o = 32;   // owner segment of this lane's candidate (32 = none)
             if (c < total) {
-                int o = 0;
+                o = 0;
 #pragma unroll
                 for (int step = 16; step; step >>= 1)
                     if (s_start[wib][o + step] <= c) o += step;
@@ -258,17 +281,19 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                 const int64_t j = s_u0[wib][1][o] + (int64_t)(t % ey);
                 const int64_t k = s_u0[wib][2][o] + (int64_t)(t / ey);
                 Fib fo;
+                float dv[3];
                 for (int ax = 0; ax < 3; ax++) {
                     fo.a[ax] = s_f[wib][ax][o];
                     fo.w[ax] = s_f[wib][3 + ax][o];
                     fo.iota[ax] = s_f[wib][6 + ax][o];
+                    dv[ax] = s_f[wib][12 + ax][o];
                 }
                 fo.r2 = s_f[wib][9][o];
                 fo.moving = __float_as_uint(s_f[wib][10][o]);
                 fo.len = s_f[wib][11][o];
                 float ell;
-                if (fiber_key(fo, i, j, k, ell)) {
-                    atomicAdd(&s_acc[wib][o], (unsigned long long)q32(ell));
+                if (!far_from_capsule(fo, dv, s_f[wib][15][o], i, j, k) && fiber_key(fo, i, j, k, ell)) {
+                    qv = q32(ell);
                     if (i >= 0 && j >= 0 && k >= 0 && i < g.N && j < g.N && k < g.N) {
                         mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
                         const uint64_t cell = mkey >> sh.shift;
@@ -279,6 +304,16 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                     }
                 }
             }
+            // exact S_acc: segmented inclusive scan over lanes of the same segment (owners are
+            // non-decreasing along the lanes), then one plain add by each segment's last lane
+#pragma unroll
+            for (int dlt = 1; dlt < 32; dlt <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, qv, dlt);
+                const int oy = __shfl_up_sync(0xffffffffu, o, dlt);
+                if (lane >= dlt && oy == o) qv += y;
+            }
+            const int onext = __shfl_down_sync(0xffffffffu, o, 1);
+            if (o < 32 && (lane == 31 || onext != o)) s_acc[wib][o] += (unsigned long long)qv;
             const unsigned bal = __ballot_sync(0xffffffffu, emit);
             if (bal) {
                 unsigned long long base = 0;
@@ -290,6 +325,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                     else atomicOr(flags, VOX_EFLAG_OVERFLOW);
                 }
             }
+            __syncwarp();
         }
         __syncwarp();
         if (p < S) {

@@ -44,142 +44,519 @@ void upload_theta(vox_ctx* c) {
     cudaMemcpyToSymbolAsync(c_coef, coef, sizeof(coef), 0, cudaMemcpyHostToDevice, c->stream);
 }
 
-// sigma_k of a lobe given by its 7 accumulators (w, M6)
-__device__ __forceinline__ float lobe_sigma(const long long* a, int k) {
-    const float wf = deq32(a[0]);
-    float q = c_coef[k][0] * (deq32(a[1]) / wf);
+constexpr unsigned INF_BITS = 0x7f800000u;
+
+// pair index t = j(j-1)/2 + i for i < j (pairs with j < n are the prefix t < n(n-1)/2)
+__device__ __forceinline__ int pair_t(int i, int j) { return j * (j - 1) / 2 + i; }
+
+// ---------------------------------------------------------------- per-level prep
+// One thread per parent: exact naive aggregate, fp32 copies, the number n of
+// dendrogram leaves (children's lobes with w != 0, D17). Parents with n <= K are final here
+// (their lobes are copied in child-slot order); the others are counted per n so that the
+// SGGX-H kernels get them grouped by n (uniform work per warp).
+template <int K>
+__global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* __restrict__ cacc,
+                           const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc, int leaf,
+                           const uint32_t* __restrict__ start, uint64_t V, uint64_t* __restrict__ pkey,
+                           long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
+                           uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+                           uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
+    constexpr int MAXN = 8 * K;
+    __shared__ unsigned s_hist[MAXN + 1];
+    for (int x = threadIdx.x; x <= MAXN; x += blockDim.x) s_hist[x] = 0;
+    __syncthreads();
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < V; p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c0 = start[p], c1 = start[p + 1];
+        long long sum[7] = {0, 0, 0, 0, 0, 0, 0};
+        int n = 0;
+        for (uint32_t x = c0; x < c1; x++) {
 #pragma unroll
-    for (int e = 1; e < 6; e++) q = q + c_coef[k][e] * (deq32(a[1 + e]) / wf);
-    return sqrtf(pmax(q, 0.0f));
+            for (int e = 0; e < 7; e++) sum[e] += cacc[7 * (uint64_t)x + e];
+            if (leaf) n += cacc[7 * (uint64_t)x] > 0;
+            else
+                for (int q = 0; q < cncl[x]; q++) n += cclacc[((uint64_t)x * K + q) * 7] != 0;
+        }
+        pkey[p] = ckey[c0] >> 3;
+#pragma unroll
+        for (int e = 0; e < 7; e++) pacc[7 * p + e] = sum[e];
+        pmass[p] = deq32(sum[0]);
+#pragma unroll
+        for (int e = 0; e < 6; e++) pm6[6 * p + e] = deq32(sum[1 + e]);
+        nlob[p] = (uint8_t)n;
+        if (n <= K) {
+            int slot = 0;
+            for (uint32_t x = c0; x < c1; x++) {
+                if (leaf) {
+                    if (cacc[7 * (uint64_t)x] > 0) {
+                        for (int e = 0; e < 7; e++) {
+                            const long long v = cacc[7 * (uint64_t)x + e];
+                            pclacc[(p * K + slot) * 7 + e] = v;
+                            pcl[(p * K + slot) * 7 + e] = deq32(v);
+                        }
+                        slot++;
+                    }
+                } else {
+                    for (int q = 0; q < cncl[x]; q++) {
+                        const long long* src = cclacc + ((uint64_t)x * K + q) * 7;
+                        if (src[0] == 0) continue;
+                        for (int e = 0; e < 7; e++) {
+                            pclacc[(p * K + slot) * 7 + e] = src[e];
+                            pcl[(p * K + slot) * 7 + e] = deq32(src[e]);
+                        }
+                        slot++;
+                    }
+                }
+            }
+            for (int q = slot; q < K; q++)
+                for (int e = 0; e < 7; e++) {
+                    pclacc[(p * K + q) * 7 + e] = 0;
+                    pcl[(p * K + q) * 7 + e] = 0.0f;
+                }
+            pncl[p] = (uint8_t)slot;
+        } else {
+            atomicAdd(&s_hist[n], 1u);
+        }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x <= MAXN; x += blockDim.x)
+        if (s_hist[x]) atomicAdd(&hist[x], s_hist[x]);
 }
 
-// d(i,j): |sigma_i - sigma_j| summed in the fixed xor-butterfly tree order (PREDICATES §9)
-__device__ __forceinline__ float lobe_dist(const float* si, const float* sj) {
-    float s[32];
+// Exclusive offsets of the per-n buckets (ascending n) and the split between the quad
+// kernel (n <= 8) and the warp kernel (n > 8). counts = {n_small, n_total}.
+__global__ void k_bucket_init(const unsigned* __restrict__ hist, int K, int maxn, unsigned* __restrict__ cursor,
+                              unsigned* __restrict__ counts) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned off = 0, small = 0;
+    for (int n = K + 1; n <= maxn; n++) {
+        cursor[n] = off;
+        off += hist[n];
+        if (n <= 8) small = off;
+    }
+    counts[0] = small;
+    counts[1] = off;
+}
+
+constexpr int SCATTER_PER_THREAD = 8;
+
+// Hard parents (n > K) into their bucket; block-local counting keeps global atomics per bin.
+__global__ void k_bucket_scatter(const uint8_t* __restrict__ nlob, uint64_t V, int K, int maxn,
+                                 unsigned* __restrict__ cursor, uint32_t* __restrict__ list) {
+    __shared__ unsigned s_cnt[65], s_base[65];
+    for (int x = threadIdx.x; x <= maxn; x += blockDim.x) s_cnt[x] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * blockDim.x * SCATTER_PER_THREAD;
+    uint8_t nn[SCATTER_PER_THREAD];
 #pragma unroll
-    for (int k = 0; k < 32; k++) s[k] = fabsf(si[k] - sj[k]);
+    for (int r = 0; r < SCATTER_PER_THREAD; r++) {
+        const uint64_t p = base + (uint64_t)r * blockDim.x + threadIdx.x;
+        nn[r] = p < V ? nlob[p] : 0;
+        if (nn[r] > K) atomicAdd(&s_cnt[nn[r]], 1u);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x <= maxn; x += blockDim.x) {
+        s_base[x] = s_cnt[x] ? atomicAdd(&cursor[x], s_cnt[x]) : 0;
+        s_cnt[x] = 0;
+    }
+    __syncthreads();
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1)
+    for (int r = 0; r < SCATTER_PER_THREAD; r++) {
+        if (nn[r] > K) {
+            const uint64_t p = base + (uint64_t)r * blockDim.x + threadIdx.x;
+            list[s_base[nn[r]] + atomicAdd(&s_cnt[nn[r]], 1u)] = (uint32_t)p;
+        }
+    }
+}
+
+// Dendrogram leaves of parent p (levels >= 2): children's stored lobes in child-slot order,
+// w = 0 dropped (D17). One lane per (child, lobe slot) -- 8 children x K slots <= 32 lanes
+// for K <= 4, looped otherwise -- compacted by ballot so the order is exactly the serial one.
+template <int K>
+__device__ __forceinline__ int gather_lobes(const uint32_t* __restrict__ start, const uint8_t* __restrict__ cncl,
+                                            const long long* __restrict__ cclacc, uint64_t p, int lane,
+                                            unsigned mask, long long* out) {
+    const uint32_t c0 = start[p], c1 = start[p + 1];
+    const int slots = (int)(c1 - c0) * K;
+    int n = 0;
+    for (int b = 0; b < 8 * K; b += 32) {
+        const int sl = b + lane;
+        bool has = false;
+        const long long* src = nullptr;
+        if (sl < slots) {
+            const uint64_t x = c0 + sl / K;
+            const int q = sl % K;
+            src = cclacc + (x * K + q) * 7;
+            has = q < cncl[x] && src[0] != 0;
+        }
+        const unsigned bal = __ballot_sync(mask, has);
+        if (has) {
+            const int c = n + __popc(bal & ((1u << lane) - 1u));
 #pragma unroll
-        for (int l = 0; l < h; l++) s[l] = s[l] + s[l + h];
-    return s[0];
+            for (int e = 0; e < 7; e++) out[7 * c + e] = src[e];
+        }
+        n += __popc(bal);
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------- SGGX-H, n <= 8 ("quad")
+// Four parents per warp, eight lanes per parent. Lane l of a group owns slices l, l+8,
+// l+16, l+24 of every lobe's sigma (registers). A distance is formed as the pinned tree
+// pairs it -- s[l] = d[l] + d[l+16], s[l+8] = d[l+8] + d[l+24], s[l] = s[l] + s[l+8] in
+// registers, then the last three tree levels by xor-shuffles inside the group -- and kept in
+// a shared 28-entry table per parent; the lexicographic argmin (d, i, j) is a group reduce.
+constexpr int QUAD_WARPS = 4;
+
+__device__ __forceinline__ float part4(const float* a, const float* b) {
+    return (fabsf(a[0] - b[0]) + fabsf(a[2] - b[2])) + (fabsf(a[1] - b[1]) + fabsf(a[3] - b[3]));
+}
+__device__ __forceinline__ float group_sum8(float s) {
+    s = s + __shfl_xor_sync(0xffffffffu, s, 4);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 2);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+__device__ __forceinline__ unsigned long long group_min8(unsigned long long v) {
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y < v ? y : v;
+    }
+    return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(QUAD_WARPS * 32)
+k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
+             const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
+             const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
+             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl) {
+    __shared__ long long s_lobe[QUAD_WARPS][4][8][7];
+    __shared__ float s_S[QUAD_WARPS][4][8][6];
+    __shared__ float s_D[QUAD_WARPS][4][28];
+    __shared__ uint16_t s_pair[28];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int l = lane & 7, g = lane >> 3;
+    if (threadIdx.x < 28) {
+        int j = 1;
+        while ((j + 1) * j / 2 <= (int)threadIdx.x) j++;
+        s_pair[threadIdx.x] = (uint16_t)((((int)threadIdx.x - j * (j - 1) / 2) << 8) | j);
+    }
+    __syncthreads();
+    long long(*lobe)[7] = s_lobe[wib][g];
+    float(*Sg)[6] = s_S[wib][g];
+    float* D = s_D[wib][g];
+    float cf[4][6];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int e = 0; e < 6; e++) cf[q][e] = c_coef[l + 8 * q][e];
+    const unsigned small = counts[0];
+    const unsigned nquad = (small + 3) / 4;
+    for (unsigned qd = blockIdx.x * QUAD_WARPS + wib; qd < nquad; qd += gridDim.x * QUAD_WARPS) {
+        const unsigned idx = 4 * qd + g;
+        const bool valid = idx < small;
+        const uint32_t p = valid ? list[idx] : 0;
+        int n = 0;
+        if (leaf) {
+            uint32_t c0 = 0;
+            int nch = 0;
+            if (valid) {
+                c0 = start[p];
+                nch = (int)(start[p + 1] - c0);
+            }
+            const bool has = l < nch && cacc[7 * (uint64_t)(c0 + l)] > 0;
+            const unsigned gm = (__ballot_sync(0xffffffffu, has) >> (8 * g)) & 0xffu;
+            n = __popc(gm);
+            if (has) {
+                const int c = __popc(gm & ((1u << l) - 1u));
+#pragma unroll
+                for (int e = 0; e < 7; e++) lobe[c][e] = cacc[7 * (uint64_t)(c0 + l) + e];
+            }
+        } else {
+            // 8 lanes x (child, lobe slot) rounds; n <= 8 here
+            n = 0;
+            uint32_t c0 = 0, c1 = 0;
+            if (valid) {
+                c0 = start[p];
+                c1 = start[p + 1];
+            }
+            const int slots = (int)(c1 - c0) * K;
+            for (int b = 0; b < 8 * K; b += 8) {
+                const int sl = b + l;
+                bool has = false;
+                const long long* src = nullptr;
+                if (sl < slots) {
+                    const uint64_t x = c0 + sl / K;
+                    const int q = sl % K;
+                    src = cclacc + (x * K + q) * 7;
+                    has = q < cncl[x] && src[0] != 0;
+                }
+                const unsigned gm = (__ballot_sync(0xffffffffu, has) >> (8 * g)) & 0xffu;
+                if (has) {
+                    const int c = n + __popc(gm & ((1u << l) - 1u));
+#pragma unroll
+                    for (int e = 0; e < 7; e++) lobe[c][e] = src[e];
+                }
+                n += __popc(gm);
+            }
+        }
+        __syncwarp();
+        const int nmax = __reduce_max_sync(0xffffffffu, valid ? n : 0);
+        if (valid && l < n) {
+            const float wf = deq32(lobe[l][0]);
+#pragma unroll
+            for (int e = 0; e < 6; e++) Sg[l][e] = deq32(lobe[l][1 + e]) / wf;
+        }
+        __syncwarp();
+        float sg[8][4];
+#pragma unroll
+        for (int c = 0; c < 8; c++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                float qq = 0.0f;
+                if (c < nmax && valid && c < n) {
+                    qq = cf[q][0] * Sg[c][0];
+#pragma unroll
+                    for (int e = 1; e < 6; e++) qq = qq + cf[q][e] * Sg[c][e];
+                }
+                sg[c][q] = (c < nmax) ? sqrtf(pmax(qq, 0.0f)) : 0.0f;
+            }
+#pragma unroll
+        for (int j = 1; j < 8; j++) {
+            if (j >= nmax) break;
+#pragma unroll
+            for (int i = 0; i < j; i++) {
+                const float s2 = group_sum8(part4(sg[i], sg[j]));
+                const int t = j * (j - 1) / 2 + i;
+                if (l == (t & 7)) D[t] = (valid && j < n) ? s2 : __uint_as_float(INF_BITS);
+            }
+        }
+        __syncwarp();
+        unsigned alive = (1u << n) - 1u;
+        const int np = nmax * (nmax - 1) / 2;
+        for (int m = nmax; m > K; m--) {
+            const bool act = valid && __popc(alive) > K;
+            unsigned long long best = ~0ull;
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const int t = l + 8 * r;
+                if (t < np) {
+                    const unsigned long long key = ((unsigned long long)__float_as_uint(D[t]) << 32) | s_pair[t];
+                    best = key < best ? key : best;
+                }
+            }
+            best = group_min8(best);
+            const int bi = (int)((best >> 8) & 0xff), bj = (int)(best & 0xff);
+            if (act && l < 7) lobe[bi][l] += lobe[bj][l];   // exact moment merge (D15)
+            __syncwarp();
+            if (act && l < 6) Sg[bi][l] = deq32(lobe[bi][1 + l]) / deq32(lobe[bi][0]);
+            __syncwarp();
+            float sn[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                float qq = 0.0f;
+                if (act) {
+                    qq = cf[q][0] * Sg[bi][0];
+#pragma unroll
+                    for (int e = 1; e < 6; e++) qq = qq + cf[q][e] * Sg[bi][e];
+                }
+                sn[q] = sqrtf(pmax(qq, 0.0f));
+            }
+#pragma unroll
+            for (int c = 0; c < 8; c++)
+                if (act && c == bi) {
+#pragma unroll
+                    for (int q = 0; q < 4; q++) sg[c][q] = sn[q];
+                }
+            if (act) alive &= ~(1u << bj);
+            float mine = 0.0f;
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                if (x >= nmax) break;
+                const float v = group_sum8(part4(sn, sg[x]));
+                if (l == x) mine = v;
+            }
+            if (act && l < n) {
+                if (l != bi && ((alive >> l) & 1u)) D[l < bi ? pair_t(l, bi) : pair_t(bi, l)] = mine;
+                if (l != bj) D[l < bj ? pair_t(l, bj) : pair_t(bj, l)] = __uint_as_float(INF_BITS);
+            }
+            __syncwarp();
+        }
+        if (valid) {
+            int slot = 0;
+            for (int c = 0; c < n; c++) {
+                if (!((alive >> c) & 1u)) continue;
+                if (l < 7) {
+                    const long long v = lobe[c][l];
+                    pclacc[((uint64_t)p * K + slot) * 7 + l] = v;
+                    pcl[((uint64_t)p * K + slot) * 7 + l] = deq32(v);
+                }
+                slot++;
+            }
+            for (int q = slot; q < K; q++)
+                if (l < 7) {
+                    pclacc[((uint64_t)p * K + q) * 7 + l] = 0;
+                    pcl[((uint64_t)p * K + q) * 7 + l] = 0.0f;
+                }
+            if (l == 0) pncl[p] = (uint8_t)slot;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- SGGX-H, n > 8 (one warp per parent)
+// d(i,j) tree for 32 slices held one per lane, for 32 pairs at once ("transpose-reduce"):
+// lane p ends with the sum for pair p. At step h a lane keeps the half of its vector whose
+// pair index has bit h equal to its own and adds the partner's partial; the partial sums it
+// adds are s[l] and s[l+h] of the pinned tree (PREDICATES §9), so the result is bit-identical
+// to the sequential tree (fp32 addition is commutative).
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int q = 0; q < h; q++) {
+            const float send = up ? v[q] : v[q + h];
+            const float keep = up ? v[q + h] : v[q];
+            v[q] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+    return v[0];
 }
 
 constexpr int LOD_WARPS = 4;
-constexpr int SIG_STRIDE = 33;   // padded sigma rows: lanes reading distinct rows hit distinct banks
+constexpr int SIG_STRIDE = 40;   // sigma rows: 4 groups x 8 lanes reading 4 rows hit 32 distinct banks
 
 template <int K>
 struct LodSmem {
     static constexpr int MAXN = 8 * K;
+    static constexpr int MAXP = MAXN * (MAXN - 1) / 2;
     static constexpr size_t list_bytes = MAXN * 7 * sizeof(long long);
+    static constexpr size_t S_bytes = ((MAXN * 6 * sizeof(float) + 15) / 16) * 16;
     static constexpr size_t sig_bytes = MAXN * SIG_STRIDE * sizeof(float);
-    static constexpr size_t dist_bytes = MAXN * MAXN * sizeof(float);
-    static constexpr size_t per_warp = list_bytes + sig_bytes + dist_bytes;
+    static constexpr size_t D_bytes = ((MAXP * sizeof(float) + 15) / 16) * 16;
+    static constexpr size_t per_warp = list_bytes + S_bytes + sig_bytes + D_bytes;
+    static constexpr size_t pairs_bytes = ((MAXP * sizeof(uint16_t) + 15) / 16) * 16;
+    static constexpr size_t total = pairs_bytes + LOD_WARPS * per_warp;
 };
 
 template <int K>
 __global__ void __launch_bounds__(LOD_WARPS * 32)
-k_pyramid(const uint64_t* __restrict__ ckey, const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
-          const long long* __restrict__ cclacc, int child_is_leaf, const uint32_t* __restrict__ start, uint64_t V,
-          uint64_t* __restrict__ pkey, long long* __restrict__ pacc, uint8_t* __restrict__ pncl,
-          long long* __restrict__ pclacc) {
+k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
+             const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc,
+             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
+             float* __restrict__ pcl) {
     using SM = LodSmem<K>;
-    constexpr int MAXN = SM::MAXN;
+    constexpr int MAXP = SM::MAXP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t* ptab = reinterpret_cast<uint16_t*>(smem_raw);   // t -> (i << 8) | j
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* base = smem_raw + wib * SM::per_warp;
-    long long(*list)[7] = reinterpret_cast<long long(*)[7]>(base);
-    float(*sig)[SIG_STRIDE] = reinterpret_cast<float(*)[SIG_STRIDE]>(base + SM::list_bytes);
-    float(*dist)[MAXN] = reinterpret_cast<float(*)[MAXN]>(base + SM::list_bytes + SM::sig_bytes);
-
-    for (uint64_t p = blockIdx.x * (uint64_t)LOD_WARPS + wib; p < V; p += (uint64_t)gridDim.x * LOD_WARPS) {
-        const uint32_t c0 = start[p], c1 = start[p + 1];
-        const int nch = (int)(c1 - c0);
-        // naive aggregate: exact sums of the children's accumulators
-        if (lane < 7) {
-            long long s = 0;
-            for (uint32_t x = c0; x < c1; x++) s += cacc[7 * (uint64_t)x + lane];
-            pacc[7 * p + lane] = s;
-        }
-        if (lane == 0) pkey[p] = ckey[c0] >> 3;
-        // dendrogram leaves: the children's lobes in child-slot order, w = 0 dropped (D17)
-        int cnt = 0;
-        if (lane < nch) {
-            const uint64_t x = c0 + lane;
-            if (child_is_leaf) cnt = cacc[7 * x] > 0;
-            else
-                for (int q = 0; q < cncl[x]; q++) cnt += cclacc[(x * K + q) * 7] != 0;
-        }
-        int incl = cnt;
+    for (int t = threadIdx.x; t < MAXP; t += blockDim.x) {
+        int j = 1;
+        while ((j + 1) * j / 2 <= t) j++;
+        ptab[t] = (uint16_t)(((t - j * (j - 1) / 2) << 8) | j);
+    }
+    __syncthreads();
+    unsigned char* base = smem_raw + SM::pairs_bytes + wib * SM::per_warp;
+    long long(*list_)[7] = reinterpret_cast<long long(*)[7]>(base);
+    float(*Sm)[6] = reinterpret_cast<float(*)[6]>(base + SM::list_bytes);
+    float(*sig)[SIG_STRIDE] = reinterpret_cast<float(*)[SIG_STRIDE]>(base + SM::list_bytes + SM::S_bytes);
+    float* D = reinterpret_cast<float*>(base + SM::list_bytes + SM::S_bytes + SM::sig_bytes);
+    float cf[6];
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int n = __shfl_sync(0xffffffffu, incl, 7);
-        if (lane < nch && cnt) {
-            const uint64_t x = c0 + lane;
-            int o = incl - cnt;
-            if (child_is_leaf) {
-                for (int e = 0; e < 7; e++) list[o][e] = cacc[7 * x + e];
-            } else {
-                for (int q = 0; q < cncl[x]; q++) {
-                    const long long* src = cclacc + (x * K + q) * 7;
-                    if (src[0] == 0) continue;
-                    for (int e = 0; e < 7; e++) list[o][e] = src[e];
-                    o++;
-                }
-            }
-        }
+    for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
+    const int l8 = lane & 7, g4 = lane >> 3;
+    const unsigned lo = counts[0], hi = counts[1];
+    for (unsigned w = lo + blockIdx.x * LOD_WARPS + wib; w < hi; w += gridDim.x * LOD_WARPS) {
+        const uint64_t p = list[w];
+        // dendrogram leaves in child-slot order, w = 0 dropped (D17)
+        // one lane per (child, lobe slot): a single round of loads, compacted by ballot
+        const int n = gather_lobes<K>(start, cncl, cclacc, p, lane, 0xffffffffu, &list_[0][0]);
         __syncwarp();
         unsigned long long alive = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
-        if (n > K) {
-            // SGGX-H: merge the closest pair until K lobes remain
-            for (int cc = 0; cc < n; cc++) sig[cc][lane] = lobe_sigma(list[cc], lane);
-            __syncwarp();
-            for (int i = 0; i + 1 < n; i++)
-                for (int j = i + 1 + lane; j < n; j += 32) dist[i][j] = lobe_dist(sig[i], sig[j]);
-            __syncwarp();
-            for (int m = n; m > K; m--) {
-                // first minimum of d over i < j in row-major order (D18): lexicographic (d, i, j)
-                unsigned long long best = ~0ull;
-                for (int i = 0; i + 1 < n; i++) {
-                    if (!((alive >> i) & 1ull)) continue;
-                    for (int j = i + 1 + lane; j < n; j += 32) {
-                        if (!((alive >> j) & 1ull)) continue;
-                        const unsigned long long key =
-                            ((unsigned long long)__float_as_uint(dist[i][j]) << 32) | (unsigned)(i << 8) | (unsigned)j;
-                        best = key < best ? key : best;
-                    }
-                }
+        // ---- S = M / w per lobe (one lane per lobe), sigma_k per lobe (one lane per slice)
+        for (int c = lane; c < n; c += 32) {
+            const float wf = deq32(list_[c][0]);
 #pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) {
-                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
-                    best = y < best ? y : best;
-                }
-                const int bi = (int)((best >> 8) & 0xff), bj = (int)(best & 0xff);
-                if (lane < 7) list[bi][lane] += list[bj][lane];   // exact moment merge (D15)
-                alive &= ~(1ull << bj);
-                __syncwarp();
-                sig[bi][lane] = lobe_sigma(list[bi], lane);
-                __syncwarp();
-                for (int x = lane; x < n; x += 32) {
-                    if (x == bi || !((alive >> x) & 1ull)) continue;
-                    const int a = x < bi ? x : bi, b = x < bi ? bi : x;
-                    dist[a][b] = lobe_dist(sig[a], sig[b]);
-                }
-                __syncwarp();
-            }
+            for (int e = 0; e < 6; e++) Sm[c][e] = deq32(list_[c][1 + e]) / wf;
         }
-        // output: surviving lobes in list order, zero-filled to K slots
+        __syncwarp();
+        for (int c = 0; c < n; c++) {
+            float q = cf[0] * Sm[c][0];
+#pragma unroll
+            for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[c][e];
+            sig[c][lane] = sqrtf(pmax(q, 0.0f));
+        }
+        __syncwarp();
+        // ---- initial distance matrix, 32 pairs per pass (lane = slice, transpose-reduce)
+        const int np = n * (n - 1) / 2;
+        for (int b = 0; b < np; b += 32) {
+            float v[32];
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+                const int t = b + q;
+                if (t < np) {
+                    const int pr = ptab[t];
+                    v[q] = fabsf(sig[pr >> 8][lane] - sig[pr & 0xff][lane]);
+                } else {
+                    v[q] = 0.0f;
+                }
+            }
+            const float d = transpose_reduce32(v, lane);
+            if (b + lane < np) D[b + lane] = d;
+        }
+        __syncwarp();
+        // ---- SGGX-H merges: argmin of d over i < j, first in row-major order (D18)
+        for (int m = n; m > K; m--) {
+            unsigned bd = 0xffffffffu, bij = 0xffffffffu;
+            for (int t = lane; t < np; t += 32) {
+                const unsigned dd = __float_as_uint(D[t]);
+                const unsigned ij = ptab[t];
+                if (dd < bd || (dd == bd && ij < bij)) { bd = dd; bij = ij; }
+            }
+            const unsigned dmin = __reduce_min_sync(0xffffffffu, bd);
+            const unsigned ijmin = __reduce_min_sync(0xffffffffu, bd == dmin ? bij : 0xffffffffu);
+            const int bi = (int)(ijmin >> 8), bj = (int)(ijmin & 0xff);
+            if (lane < 7) list_[bi][lane] += list_[bj][lane];   // exact moment merge (D15)
+            alive &= ~(1ull << bj);
+            __syncwarp();
+            if (lane < 6) Sm[bi][lane] = deq32(list_[bi][1 + lane]) / deq32(list_[bi][0]);
+            __syncwarp();
+            {
+                float q = cf[0] * Sm[bi][0];
+#pragma unroll
+                for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[bi][e];
+                sig[bi][lane] = sqrtf(pmax(q, 0.0f));
+            }
+            __syncwarp();
+            // new row d(bi, x): 8 lanes per pair (lane l sums slices l, l+8, l+16, l+24 in the
+            // first two tree levels), then the last three levels by xor-shuffles in the group
+            for (int x0 = 0; x0 < n; x0 += 4) {
+                const int x = x0 + g4;
+                const int xr = x < n ? x : bi;
+                float s0 = fabsf(sig[bi][l8] - sig[xr][l8]) + fabsf(sig[bi][l8 + 16] - sig[xr][l8 + 16]);
+                float s1 = fabsf(sig[bi][l8 + 8] - sig[xr][l8 + 8]) + fabsf(sig[bi][l8 + 24] - sig[xr][l8 + 24]);
+                const float s = group_sum8(s0 + s1);
+                if (l8 == 0 && x < n && x != bi && ((alive >> x) & 1ull))
+                    D[x < bi ? pair_t(x, bi) : pair_t(bi, x)] = s;
+            }
+            // retire every pair of bj
+            for (int x = lane; x < n; x += 32)
+                if (x != bj) D[x < bj ? pair_t(x, bj) : pair_t(bj, x)] = __uint_as_float(INF_BITS);
+            __syncwarp();
+        }
+        // output: surviving lobes in list order (K slots exactly, since n > K)
         int slot = 0;
         for (int cc = 0; cc < n; cc++) {
             if (!((alive >> cc) & 1ull)) continue;
-            if (lane < 7) pclacc[(p * K + slot) * 7 + lane] = list[cc][lane];
+            if (lane < 7) {
+                const long long a = list_[cc][lane];
+                pclacc[(p * K + slot) * 7 + lane] = a;
+                pcl[(p * K + slot) * 7 + lane] = deq32(a);
+            }
             slot++;
         }
-        for (int q = slot; q < K; q++)
-            if (lane < 7) pclacc[(p * K + q) * 7 + lane] = 0;
         if (lane == 0) pncl[p] = (uint8_t)slot;
         __syncwarp();
     }
@@ -239,16 +616,46 @@ cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters) {
     } while (0)
 
 template <int K>
-static cudaError_t launch_pyramid(vox_ctx* c, const Level& C, int child_is_leaf, const uint32_t* start, Level& P) {
-    const size_t smem = LodSmem<K>::per_warp * LOD_WARPS;
-    cudaError_t e = cudaFuncSetAttribute(k_pyramid<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    uint64_t blocks = (P.n + LOD_WARPS - 1) / LOD_WARPS;
-    if (blocks > 148ull * 64) blocks = 148ull * 64;
-    k_pyramid<K><<<(unsigned)blocks, LOD_WARPS * 32, smem, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, child_is_leaf,
-                                                                       start, P.n, P.key, P.acc, P.ncl, P.clacc);
-    c->st.launches++;
-    return cudaGetLastError();
+static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t* start, Level& P) {
+    constexpr int MAXN = 8 * K;
+    const uint64_t V = P.n;
+    uint8_t* nlob = nullptr;
+    unsigned *hist = nullptr, *cursor = nullptr, *counts = nullptr;
+    uint32_t* list = nullptr;
+    CK(dalloc(c, (void**)&nlob, V));
+    CK(dalloc(c, (void**)&hist, 4 * (MAXN + 1) * 2 + 16));
+    cursor = hist + (MAXN + 1);
+    counts = cursor + (MAXN + 1);
+    CK(dalloc(c, (void**)&list, V * 4));
+    CK(cudaMemsetAsync(hist, 0, 4 * (MAXN + 1), c->stream));
+    k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, leaf, start, V, P.key, P.acc,
+                                                     P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
+    k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts);
+    const uint64_t sb = (V + 256ull * SCATTER_PER_THREAD - 1) / (256ull * SCATTER_PER_THREAD);
+    k_bucket_scatter<<<(unsigned)(sb ? sb : 1), 256, 0, c->stream>>>(nlob, V, K, MAXN, cursor, list);
+    c->st.launches += 3;
+    // grids cover the worst case (every parent hard); blocks stride over the actual counts
+    if (K < 8) {
+        uint64_t qb = ((V + 3) / 4 + QUAD_WARPS - 1) / QUAD_WARPS;
+        qb = std::min<uint64_t>(std::max<uint64_t>(qb, 1), 148ull * 48);
+        k_sggxh_quad<K><<<(unsigned)qb, QUAD_WARPS * 32, 0, c->stream>>>(list, counts, C.acc, C.ncl, C.clacc, leaf,
+                                                                        start, P.ncl, P.clacc, P.cl);
+        c->st.launches++;
+    }
+    if (!leaf && MAXN > 8) {
+        const size_t smem = LodSmem<K>::total;
+        CK(cudaFuncSetAttribute(k_sggxh_warp<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        uint64_t wb = (V + LOD_WARPS - 1) / LOD_WARPS;
+        wb = std::min<uint64_t>(std::max<uint64_t>(wb, 1), 148ull * 32);
+        k_sggxh_warp<K><<<(unsigned)wb, LOD_WARPS * 32, smem, c->stream>>>(list, counts, C.ncl, C.clacc, start,
+                                                                          P.ncl, P.clacc, P.cl);
+        c->st.launches++;
+    }
+    CK(cudaGetLastError());
+    dfree(c, list);
+    dfree(c, hist);
+    dfree(c, nlob);
+    return VOX_OK;
 }
 
 vox_status build_level(vox_ctx* c, int l) {
@@ -269,7 +676,7 @@ vox_status build_level(vox_ctx* c, int l) {
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flags, incl, (int64_t)n, c->stream));
     CK(dalloc(c, &tmp, tb));
     CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
-    c->st.launches++;
+    c->st.launches += 2;
     uint32_t V = 0;
     CK(cudaMemcpyAsync(&V, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -290,22 +697,20 @@ vox_status build_level(vox_ctx* c, int l) {
     CK(dalloc(c, (void**)&P.cl, (uint64_t)V * K * 28));
     timer_begin(c, c->t_lod);
     const int leaf = (l == 1);
-    cudaError_t e;
+    vox_status s;
     switch (K) {
-        case 1: e = launch_pyramid<1>(c, C, leaf, start, P); break;
-        case 2: e = launch_pyramid<2>(c, C, leaf, start, P); break;
-        case 3: e = launch_pyramid<3>(c, C, leaf, start, P); break;
-        case 4: e = launch_pyramid<4>(c, C, leaf, start, P); break;
-        case 5: e = launch_pyramid<5>(c, C, leaf, start, P); break;
-        case 6: e = launch_pyramid<6>(c, C, leaf, start, P); break;
-        case 7: e = launch_pyramid<7>(c, C, leaf, start, P); break;
-        default: e = launch_pyramid<8>(c, C, leaf, start, P); break;
+        case 1: s = run_level<1>(c, C, leaf, start, P); break;
+        case 2: s = run_level<2>(c, C, leaf, start, P); break;
+        case 3: s = run_level<3>(c, C, leaf, start, P); break;
+        case 4: s = run_level<4>(c, C, leaf, start, P); break;
+        case 5: s = run_level<5>(c, C, leaf, start, P); break;
+        case 6: s = run_level<6>(c, C, leaf, start, P); break;
+        case 7: s = run_level<7>(c, C, leaf, start, P); break;
+        default: s = run_level<8>(c, C, leaf, start, P); break;
     }
-    CK(e);
     timer_end(c, c->t_lod);
     dfree(c, start);
-    CK(launch_finalize(c, P, true));
-    return VOX_OK;
+    return s;
 }
 
 // ---------------------------------------------------------------- multi-GPU level records

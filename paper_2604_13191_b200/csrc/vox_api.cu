@@ -67,8 +67,15 @@ using namespace vox;
 
 static vox_status ensure_dev(vox_ctx* c) {
     if (c->d_flags) return VOX_OK;
-    CKS(cudaMalloc((void**)&c->d_flags, 16));
-    CKS(cudaMalloc((void**)&c->d_counter, 16));
+    // keep freed stream-ordered allocations in the pool across calls (no re-mapping per step)
+    int dev = 0;
+    cudaMemPool_t pool;
+    CKS(cudaGetDevice(&dev));
+    CKS(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CKS(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CKS(cudaMallocAsync((void**)&c->d_flags, 16, c->stream));
+    CKS(cudaMallocAsync((void**)&c->d_counter, 16, c->stream));
     upload_theta(c);
     CKS(cudaGetLastError());
     return VOX_OK;
@@ -500,9 +507,9 @@ void vox_destroy(vox_ctx* c) {
         timer_flush(*t);
         if (t->open) cudaEventDestroy(t->open);
     }
+    if (c->d_flags) cudaFreeAsync(c->d_flags, c->stream);
+    if (c->d_counter) cudaFreeAsync(c->d_counter, c->stream);
     cudaStreamSynchronize(c->stream);
-    if (c->d_flags) cudaFree(c->d_flags);
-    if (c->d_counter) cudaFree(c->d_counter);
     delete c;
 }
 
