@@ -90,58 +90,61 @@ def _workload(cfg: int, n_segments: int | None):
     return c
 
 
-def _cell_sample(seg, bbox, N, level, target):
-    """Pick the Morton cell at `level` whose segment count is closest to `target`
-    (a bounded, spatially complete sample for the oracle). Returns (cell, count)."""
+def _cells_by_count(seg, bbox, N, level):
+    """Morton cells at `level` with their segment counts (by segment midpoint), largest first."""
     E = float(np.max(bbox[3:] - bbox[:3]))
     mid = 0.5 * (seg[:, 0].astype(np.float64) + seg[:, 1])
     g = np.floor((mid - bbox[:3]) / E * N).astype(np.int64) >> level
     g = np.clip(g, 0, (N >> level) - 1)
     cells = np.zeros(len(g), np.uint64)
-    for b in range(12):
+    for b in range(13):
         for a in range(3):
             cells |= ((g[:, a].astype(np.uint64) >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
     u, cnt = np.unique(cells, return_counts=True)
-    i = int(np.argmin(np.abs(cnt - target)))
-    return int(u[i]), int(cnt[i])
+    order = np.argsort(-cnt, kind="stable")
+    return u[order], cnt[order]
 
 
 def oracle_sample(c, target_segments: int, level: int):
-    """Time the oracle (single-threaded, as it stands) on one Morton-cell window: every
-    segment touching the cell is voxelized (its S_p needs all its keys) and the LoD is built
-    inside the window up to `level`. Returns (segments processed, seconds, description)."""
+    """Time the oracle (single-threaded, as it stands) on whole Morton cells at `level`,
+    largest first, until `target_segments` segments have been processed: every segment
+    touching a cell is voxelized (its S_p needs all its keys) and the LoD is built inside the
+    cell up to `level`. Returns (segments processed, seconds, description)."""
     import oracle
     seg, rad, bbox, N = c["segments"], c["radii"], c["bbox"], c["grid_res"]
-    cell, _ = _cell_sample(seg, bbox, N, level, target_segments)
-    # segments whose candidate box can touch the window (cheap host prefilter, the oracle
-    # culls exactly)
     E = float(np.max(bbox[3:] - bbox[:3]))
     lo = np.minimum(seg[:, 0], seg[:, 1]) - rad[:, None]
     hi = np.maximum(seg[:, 0], seg[:, 1]) + rad[:, None]
-    gi = [0, 0, 0]
-    import oracle as O
-    i, j, k = O.unmorton(cell)
-    box_lo = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
-    box_hi = box_lo + ((1 << level) + 4) * E / N
-    sel = np.all((hi >= box_lo) & (lo <= box_hi), axis=1)
-    s, r = np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
-    o = oracle.Oracle(N, bbox)
-    o.set_window(level, cell)
-    t0 = time.perf_counter()
-    o.add_fibers(s, r)
-    o.build(level)
-    dt = time.perf_counter() - t0
-    desc = (f"oracle (plain C, 1 thread) on Morton cell {cell} at level {level} "
-            f"({(1 << level)}^3 voxels): {len(s)} segments touching it voxelized + LoD levels 1..{level} inside it")
-    del gi
-    return len(s), dt, desc
+    cells, _ = _cells_by_count(seg, bbox, N, level)
+    done, secs, used = 0, 0.0, []
+    for cell in cells:
+        i, j, k = oracle.unmorton(int(cell))
+        box_lo = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
+        box_hi = box_lo + ((1 << level) + 4) * E / N
+        sel = np.all((hi >= box_lo) & (lo <= box_hi), axis=1)
+        s, r = np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
+        o = oracle.Oracle(N, bbox)
+        o.set_window(level, int(cell))
+        t0 = time.perf_counter()
+        o.add_fibers(s, r)
+        o.build(level)
+        secs += time.perf_counter() - t0
+        done += len(s)
+        used.append(int(cell))
+        o.close()
+        if done >= target_segments:
+            break
+    desc = (f"oracle (plain C, 1 thread) on {len(used)} Morton cell(s) at level {level} "
+            f"({1 << level}^3 voxels each): {done} segments touching them voxelized + LoD levels 1..{level} "
+            f"inside them")
+    return done, secs, desc
 
 
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores, bounded samples."""
     c = _workload(args.config, args.segments)
     lvl = 7 if c["grid_res"] >= 2048 else max(1, int(math.log2(c["grid_res"])) - 2)
-    times, counts, desc = [], [], ""
+    times, counts, desc = [], [], ""   # each step: one bounded oracle sample (~1-3 s)
     for it in range(args.warmup + args.steps):
         n, dt, desc = oracle_sample(c, args.ref_segments, lvl)
         if it >= args.warmup:
@@ -167,7 +170,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-segments", type=int, default=150_000, help="oracle sample size (cpu_baseline)")
+    ap.add_argument("--cpu-segments", type=int, default=400_000, help="oracle sample size (cpu_baseline)")
     ap.add_argument("--ref-segments", type=int, default=40_000, help="oracle sample size per reference step")
     args = ap.parse_args()
 
@@ -222,6 +225,7 @@ def main():
     stage = {}
     counts = {}
     launches = 0
+    lodwork = {"sigma": 0, "dist": 0, "hard": 0}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -229,12 +233,14 @@ def main():
             v = step(profile=True)
             st = v.stats()
             for k2 in ("ms_bound", "ms_emit", "ms_sort", "ms_reduce", "ms_merge", "ms_lod_scan", "ms_lod",
-                       "ms_total_vox", "ms_total_lod"):
+                       "ms_total_vox", "ms_total_lod", "ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_warp"):
                 stage[k2] = stage.get(k2, 0.0) + st[k2]
             launches += st["launches"]
-            counts = {"pairs": st["pairs"], "candidates": st["candidates"], "voxels": st["voxels"]}
-            if not counts.get("levels"):
-                counts["levels"] = [int(v.view(l)["n"]) for l in range(levels + 1)]
+            lodwork["sigma"] += st["lod_sigma_evals"]
+            lodwork["dist"] += st["lod_dist_evals"]
+            lodwork["hard"] += st["lod_hard_parents"]
+            counts = {"pairs": st["pairs"], "candidates": st["candidates"], "voxels": st["voxels"],
+                      "levels": [int(v.view(l)["n"]) for l in range(levels + 1)]}
             v.close()
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -253,25 +259,42 @@ def main():
     # ---------------------------------------------------------------- roofline of the dominant kernel
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    # fp32 lane-op ceiling: SMs x 128 FP32 lanes x clock (no FMA on the pinned path: 1 op per lane-cycle)
+    alu_peak_tflops = nsm * 128 * sm_mhz * 1e6 / 1e12
     V = counts["levels"]
     P = counts["pairs"]
     bytes_vox = 28 * n_prims + 32 * P + 36 * V[0]
     bytes_lod = sum((36 * V[0] if l == 1 else 121 * V[l - 1]) + 121 * V[l] for l in range(1, levels + 1))
-    kernels = {
-        "k_fiber_emit" if fib else "k_tri_emit": stage["ms_emit"],
-        "radix_sort(pairs)": stage["ms_sort"],
-        "k_segreduce": stage["ms_reduce"],
-        "k_pyramid(sggxh)": stage["ms_lod"],
+    sig_ev, dist_ev = lodwork["sigma"] / args.steps, lodwork["dist"] / args.steps
+    flops_sggxh = 416.0 * sig_ev + 95.0 * dist_ev      # PREDICATES §9: 32 x 13 per sigma, 32+32+31 per distance
+    kern = {
+        ("k_fiber_emit" if fib else "k_tri_emit"): (stage["ms_emit"], "hbm", 28 * n_prims + 16 * P + 16 * n_prims),
+        "radix_sort(pairs)": (stage["ms_sort"], "hbm", 32 * P),
+        "segmented_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
+        "k_lod_prep": (stage["ms_lod_prep"], "hbm", bytes_lod),
+        "k_sggxh_warp+quad": (stage["ms_sggxh_quad"] + stage["ms_sggxh_warp"], "alu", flops_sggxh),
     }
-    dom = max(kernels, key=kernels.get)
-    alg = {"k_fiber_emit": 28 * n_prims + 16 * P + 16 * n_prims, "k_tri_emit": 36 * n_prims + 16 * P + 16 * n_prims,
-           "radix_sort(pairs)": 32 * P, "k_segreduce": 16 * P + 16 * n_prims + 64 * V[0],
-           "k_pyramid(sggxh)": bytes_lod}[dom]
-    dur = kernels[dom] / 1e3
-    roof = {"kernel": dom, "bound": "hbm", "achieved": alg / dur / 1e9 if dur > 0 else None, "peak": hbm,
-            "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "when" in peaks else "fallback",
-            "traffic": None, "alg_bytes_per_launch": alg, "ms_per_launch": kernels[dom]}
-    roof["frac"] = roof["achieved"] / hbm if roof["achieved"] else None
+    dom = max(kern, key=lambda k: kern[k][0])
+    def roof_of(name):
+        ms_k, bound, work = kern[name]
+        dur = ms_k / 1e3
+        if bound == "hbm":
+            ach = work / dur / 1e9 if dur > 0 else None
+            r = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)", "alg_bytes_per_launch": work}
+        else:
+            ach = work / dur / 1e12 if dur > 0 else None
+            r = {"kernel": name, "bound": "alu", "achieved": ach, "peak": alu_peak_tflops, "unit": "TFLOP/s",
+                 "peak_source": f"{nsm} SMs x 128 fp32 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz; no FMA)",
+                 "alg_flops_per_launch": work}
+        r["frac"] = (r["achieved"] / r["peak"]) if r["achieved"] else None
+        r["ms_per_launch"] = ms_k
+        r["traffic"] = None
+        return r
+    roof = roof_of(dom)
+    others = {k: {kk: roof_of(k)[kk] for kk in ("bound", "achieved", "unit", "frac", "ms_per_launch")} for k in kern}
 
     line = {"metric": METRIC, "value": value, "unit": "segments/s" if fib else "triangles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -283,13 +306,15 @@ def main():
             "hbm_alg_gbs_full_build": (bytes_vox + bytes_lod) / (ms_step / 1e3) / 1e9,
             "stages_ms": {k2: round(v2, 4) for k2, v2 in stage.items()},
             "counts": {"pairs": P, "candidates": counts["candidates"], "voxels_per_level": V},
-            "roofline": roof, "gpu_launches": launches}
+            "roofline": roof, "kernels": others, "gpu_launches": launches,
+            "sggxh_work": {"sigma_evals": sig_ev, "dist_evals": dist_ev, "hard_parents": lodwork["hard"] / args.steps}}
 
     # ---------------------------------------------------------------- e2e through the C ABI, host buffers
     if not args.no_e2e:
         pa = torch.from_numpy(h_a).pin_memory()
         pb = torch.from_numpy(h_b).pin_memory() if h_b is not None else None
         outs = {}
+        host = {}
 
         def e2e_step():
             v = Vox(N, bbox, rank=rank, world=world)
@@ -299,9 +324,16 @@ def main():
                 v.voxelize_triangles_host(pa, pb)
             v.build_lod(levels, group)
             d2h = 0
-            for l in range(1, levels + 1):   # the LoD volumes delivered to the host (levels 1..L)
-                lv = v.level(l, device="cpu")
-                d2h += sum(t.numel() * t.element_size() for k3, t in lv.items() if k3 != "acc")
+            for l in range(1, levels + 1):   # the LoD volumes delivered to host memory (levels 1..L)
+                n_l = int(v.view(l)["n"])
+                if l not in host or host[l]["key"].numel() < n_l:
+                    host[l] = {"key": torch.empty(n_l, dtype=torch.int64).pin_memory(),
+                               "mass": torch.empty(n_l, dtype=torch.float32).pin_memory(),
+                               "m6": torch.empty(n_l * 6, dtype=torch.float32).pin_memory(),
+                               "ncl": torch.empty(n_l, dtype=torch.uint8).pin_memory(),
+                               "cl": torch.empty(n_l * v.k * 7, dtype=torch.float32).pin_memory()}
+                v.copy_level_to(l, host[l])
+                d2h += n_l * (8 + 4 + 24 + 1 + 28 * v.k)
             v.close()
             outs["d2h"] = d2h
 
@@ -329,7 +361,7 @@ def main():
 
     # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu_baseline and fib:
-        lvl = 7 if N >= 2048 else max(1, int(math.log2(N)) - 2)
+        lvl = 9 if N >= 4096 else max(1, int(math.log2(N)) - 3)
         n, dt, desc = oracle_sample(c, args.cpu_segments, lvl)
         line["cpu_baseline"] = {"value": n / dt, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc,
                                 "seconds": dt}

@@ -48,7 +48,9 @@ class _Stats(C.Structure):
                 ("ms_bound", C.c_double), ("ms_emit", C.c_double), ("ms_sort", C.c_double),
                 ("ms_reduce", C.c_double), ("ms_merge", C.c_double), ("ms_lod_scan", C.c_double),
                 ("ms_lod", C.c_double), ("ms_total_vox", C.c_double), ("ms_total_lod", C.c_double),
-                ("launches", C.c_uint64)]
+                ("ms_lod_prep", C.c_double), ("ms_sggxh_quad", C.c_double), ("ms_sggxh_warp", C.c_double),
+                ("launches", C.c_uint64), ("lod_sigma_evals", C.c_uint64), ("lod_dist_evals", C.c_uint64),
+                ("lod_hard_parents", C.c_uint64)]
 
 
 _lib = None
@@ -249,6 +251,13 @@ class Vox:
                     "copy_level")
         self._check(lib().vox_copy_level_acc(self._h, int(level), out["acc"].data_ptr()), "copy_level_acc")
         return out
+
+    def copy_level_to(self, level: int, out: dict):
+        """vox_copy_level into caller tensors (device or pinned host): keys key/mass/m6/ncl/cl,
+        each optional, each at least as large as the level."""
+        ptr = lambda k: out[k].data_ptr() if k in out and out[k] is not None else None
+        self._check(lib().vox_copy_level(self._h, int(level), ptr("key"), ptr("mass"), ptr("m6"), ptr("ncl"),
+                                         ptr("cl")), "copy_level")
 
     # ------------------------------------------------------------------ multi-GPU records
     def export_level(self, level: int):

@@ -49,6 +49,7 @@ constexpr unsigned INF_BITS = 0x7f800000u;
 // pair index t = j(j-1)/2 + i for i < j (pairs with j < n are the prefix t < n(n-1)/2)
 __device__ __forceinline__ int pair_t(int i, int j) { return j * (j - 1) / 2 + i; }
 
+
 // ---------------------------------------------------------------- per-level prep
 // One thread per parent: exact naive aggregate, fp32 copies, the number n of
 // dendrogram leaves (children's lobes with w != 0, D17). Parents with n <= K are final here
@@ -426,7 +427,7 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 }
 
 constexpr int LOD_WARPS = 4;
-constexpr int SIG_STRIDE = 40;   // sigma rows: 4 groups x 8 lanes reading 4 rows hit 32 distinct banks
+constexpr int SIG_STRIDE = 36;   // sigma rows (16-byte aligned): 8 distinct rows per LDS.128 wavefront
 
 template <int K>
 struct LodSmem {
@@ -435,7 +436,7 @@ struct LodSmem {
     static constexpr size_t list_bytes = MAXN * 7 * sizeof(long long);
     static constexpr size_t S_bytes = ((MAXN * 6 * sizeof(float) + 15) / 16) * 16;
     static constexpr size_t sig_bytes = MAXN * SIG_STRIDE * sizeof(float);
-    static constexpr size_t D_bytes = ((MAXP * sizeof(float) + 15) / 16) * 16;
+    static constexpr size_t D_bytes = ((MAXP * sizeof(unsigned long long) + 15) / 16) * 16;
     static constexpr size_t per_warp = list_bytes + S_bytes + sig_bytes + D_bytes;
     static constexpr size_t pairs_bytes = ((MAXP * sizeof(uint16_t) + 15) / 16) * 16;
     static constexpr size_t total = pairs_bytes + LOD_WARPS * per_warp;
@@ -462,7 +463,8 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     long long(*list_)[7] = reinterpret_cast<long long(*)[7]>(base);
     float(*Sm)[6] = reinterpret_cast<float(*)[6]>(base + SM::list_bytes);
     float(*sig)[SIG_STRIDE] = reinterpret_cast<float(*)[SIG_STRIDE]>(base + SM::list_bytes + SM::S_bytes);
-    float* D = reinterpret_cast<float*>(base + SM::list_bytes + SM::S_bytes + SM::sig_bytes);
+    // D[t] = (bits of d << 32) | (i << 8 | j): one 64-bit compare orders by (d, i, j) (D18)
+    unsigned long long* D = reinterpret_cast<unsigned long long*>(base + SM::list_bytes + SM::S_bytes + SM::sig_bytes);
     float cf[6];
 #pragma unroll
     for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
@@ -482,6 +484,7 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             for (int e = 0; e < 6; e++) Sm[c][e] = deq32(list_[c][1 + e]) / wf;
         }
         __syncwarp();
+        const int np = n * (n - 1) / 2;
         for (int c = 0; c < n; c++) {
             float q = cf[0] * Sm[c][0];
 #pragma unroll
@@ -489,32 +492,36 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             sig[c][lane] = sqrtf(pmax(q, 0.0f));
         }
         __syncwarp();
-        // ---- initial distance matrix, 32 pairs per pass (lane = slice, transpose-reduce)
-        const int np = n * (n - 1) / 2;
-        for (int b = 0; b < np; b += 32) {
-            float v[32];
+        // ---- initial distance matrix: one pair per lane, the pinned tree evaluated in
+        // registers from two 32-slice sigma rows read as float4 (PREDICATES §9)
+        for (int t = lane; t < np; t += 32) {
+            const int pr = ptab[t];
+            const float4* ri = reinterpret_cast<const float4*>(sig[pr >> 8]);
+            const float4* rj = reinterpret_cast<const float4*>(sig[pr & 0xff]);
+            float sv[32];
 #pragma unroll
-            for (int q = 0; q < 32; q++) {
-                const int t = b + q;
-                if (t < np) {
-                    const int pr = ptab[t];
-                    v[q] = fabsf(sig[pr >> 8][lane] - sig[pr & 0xff][lane]);
-                } else {
-                    v[q] = 0.0f;
-                }
+            for (int k4 = 0; k4 < 8; k4++) {
+                const float4 a = ri[k4], b = rj[k4];
+                sv[4 * k4 + 0] = fabsf(a.x - b.x);
+                sv[4 * k4 + 1] = fabsf(a.y - b.y);
+                sv[4 * k4 + 2] = fabsf(a.z - b.z);
+                sv[4 * k4 + 3] = fabsf(a.w - b.w);
             }
-            const float d = transpose_reduce32(v, lane);
-            if (b + lane < np) D[b + lane] = d;
+#pragma unroll
+            for (int h = 16; h >= 1; h >>= 1)
+#pragma unroll
+                for (int q = 0; q < h; q++) sv[q] = sv[q] + sv[q + h];
+            D[t] = ((unsigned long long)__float_as_uint(sv[0]) << 32) | (unsigned)pr;
         }
         __syncwarp();
         // ---- SGGX-H merges: argmin of d over i < j, first in row-major order (D18)
         for (int m = n; m > K; m--) {
-            unsigned bd = 0xffffffffu, bij = 0xffffffffu;
+            unsigned long long best = ~0ull;
             for (int t = lane; t < np; t += 32) {
-                const unsigned dd = __float_as_uint(D[t]);
-                const unsigned ij = ptab[t];
-                if (dd < bd || (dd == bd && ij < bij)) { bd = dd; bij = ij; }
+                const unsigned long long key = D[t];
+                best = key < best ? key : best;
             }
+            const unsigned bd = (unsigned)(best >> 32), bij = (unsigned)best;
             const unsigned dmin = __reduce_min_sync(0xffffffffu, bd);
             const unsigned ijmin = __reduce_min_sync(0xffffffffu, bd == dmin ? bij : 0xffffffffu);
             const int bi = (int)(ijmin >> 8), bj = (int)(ijmin & 0xff);
@@ -538,12 +545,17 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 float s0 = fabsf(sig[bi][l8] - sig[xr][l8]) + fabsf(sig[bi][l8 + 16] - sig[xr][l8 + 16]);
                 float s1 = fabsf(sig[bi][l8 + 8] - sig[xr][l8 + 8]) + fabsf(sig[bi][l8 + 24] - sig[xr][l8 + 24]);
                 const float s = group_sum8(s0 + s1);
-                if (l8 == 0 && x < n && x != bi && ((alive >> x) & 1ull))
-                    D[x < bi ? pair_t(x, bi) : pair_t(bi, x)] = s;
+                if (l8 == 0 && x < n && x != bi && ((alive >> x) & 1ull)) {
+                    const int a = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                    D[pair_t(a, b2)] = ((unsigned long long)__float_as_uint(s) << 32) | (unsigned)((a << 8) | b2);
+                }
             }
             // retire every pair of bj
             for (int x = lane; x < n; x += 32)
-                if (x != bj) D[x < bj ? pair_t(x, bj) : pair_t(bj, x)] = __uint_as_float(INF_BITS);
+                if (x != bj) {
+                    const int a = x < bj ? x : bj, b2 = x < bj ? bj : x;
+                    D[pair_t(a, b2)] = ((unsigned long long)INF_BITS << 32) | (unsigned)((a << 8) | b2);
+                }
             __syncwarp();
         }
         // output: surviving lobes in list order (K slots exactly, since n > K)
@@ -628,8 +640,10 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     counts = cursor + (MAXN + 1);
     CK(dalloc(c, (void**)&list, V * 4));
     CK(cudaMemsetAsync(hist, 0, 4 * (MAXN + 1), c->stream));
+    timer_begin(c, c->t_prep);
     k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, leaf, start, V, P.key, P.acc,
                                                      P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
+    timer_end(c, c->t_prep);
     k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts);
     const uint64_t sb = (V + 256ull * SCATTER_PER_THREAD - 1) / (256ull * SCATTER_PER_THREAD);
     k_bucket_scatter<<<(unsigned)(sb ? sb : 1), 256, 0, c->stream>>>(nlob, V, K, MAXN, cursor, list);
@@ -638,8 +652,10 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     if (K < 8) {
         uint64_t qb = ((V + 3) / 4 + QUAD_WARPS - 1) / QUAD_WARPS;
         qb = std::min<uint64_t>(std::max<uint64_t>(qb, 1), 148ull * 48);
+        timer_begin(c, c->t_quad);
         k_sggxh_quad<K><<<(unsigned)qb, QUAD_WARPS * 32, 0, c->stream>>>(list, counts, C.acc, C.ncl, C.clacc, leaf,
                                                                         start, P.ncl, P.clacc, P.cl);
+        timer_end(c, c->t_quad);
         c->st.launches++;
     }
     if (!leaf && MAXN > 8) {
@@ -647,11 +663,28 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         CK(cudaFuncSetAttribute(k_sggxh_warp<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         uint64_t wb = (V + LOD_WARPS - 1) / LOD_WARPS;
         wb = std::min<uint64_t>(std::max<uint64_t>(wb, 1), 148ull * 32);
+        timer_begin(c, c->t_warp);
         k_sggxh_warp<K><<<(unsigned)wb, LOD_WARPS * 32, smem, c->stream>>>(list, counts, C.ncl, C.clacc, start,
                                                                           P.ncl, P.clacc, P.cl);
+        timer_end(c, c->t_warp);
         c->st.launches++;
     }
     CK(cudaGetLastError());
+    if (c->profile) {
+        // algorithmic SGGX-H work of this level from the per-n histogram: sigma evaluations
+        // (n initial + one per merge) and distance evaluations (n(n-1)/2 initial + m-2 per
+        // merge at size m), each a pinned sequence of fp32 operations
+        std::vector<unsigned> h(MAXN + 1);
+        CK(cudaMemcpyAsync(h.data(), hist, 4 * (MAXN + 1), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int n = K + 1; n <= MAXN; n++) {
+            uint64_t sg = (uint64_t)n + (uint64_t)(n - K), dd = (uint64_t)n * (n - 1) / 2;
+            for (int m = n; m > K; m--) dd += (uint64_t)(m - 2);
+            c->st.lod_sigma_evals += (uint64_t)h[n] * sg;
+            c->st.lod_dist_evals += (uint64_t)h[n] * dd;
+            c->st.lod_hard_parents += h[n];
+        }
+    }
     dfree(c, list);
     dfree(c, hist);
     dfree(c, nlob);

@@ -104,7 +104,7 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flags, incl, (int64_t)n, c->stream));
     CK(dalloc(c, &tmp, tb));
     CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
-    c->st.launches++;
+    c->st.launches += 2;   // scan init + scan
     uint32_t V32 = 0;
     CK(cudaMemcpyAsync(&V32, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -146,7 +146,7 @@ static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, u
         CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int64_t)tot, 0, 3 * c->g.logN, c->stream));
         CK(dalloc(c, &tmp, tb));
         CK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)tot, 0, 3 * c->g.logN, c->stream));
-        c->st.launches++;
+        c->st.launches += 2 + (3 * c->g.logN + 7) / 8;
         uint32_t* start = nullptr;
         uint64_t VM = 0;
         vox_status s = find_runs(c, dk.Current(), tot, &start, &VM);
@@ -185,7 +185,7 @@ vox_status reduce_pairs(vox_ctx* c, uint64_t* keys, uint64_t* keys_alt, uint64_t
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int64_t)P, 0, 3 * c->g.logN, c->stream));
     CK(dalloc(c, &tmp, tb));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)P, 0, 3 * c->g.logN, c->stream));
-    c->st.launches++;
+    c->st.launches += 2 + (3 * c->g.logN + 7) / 8;   // histogram + exclusive sum + one onesweep pass per 8 bits
     timer_end(c, c->t_sort);
     dfree(c, tmp);
     timer_begin(c, c->t_reduce);

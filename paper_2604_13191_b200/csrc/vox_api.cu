@@ -477,6 +477,9 @@ vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     c->st.ms_lod = timer_flush(c->t_lod);
     c->st.ms_total_vox = timer_flush(c->t_vox);
     c->st.ms_total_lod = timer_flush(c->t_lodall);
+    c->st.ms_lod_prep = timer_flush(c->t_prep);
+    c->st.ms_sggxh_quad = timer_flush(c->t_quad);
+    c->st.ms_sggxh_warp = timer_flush(c->t_warp);
     *out = c->st;
     return VOX_OK;
 }
@@ -486,9 +489,10 @@ vox_status vox_stats_reset(vox_ctx* c) {
     vox_stats tmp;
     vox_stats_get(c, &tmp);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall})
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp})
         t->ms = 0.0;
     c->st.launches = 0;
+    c->st.lod_sigma_evals = c->st.lod_dist_evals = c->st.lod_hard_parents = 0;
     return VOX_OK;
 }
 
@@ -503,7 +507,7 @@ void vox_destroy(vox_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall}) {
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp}) {
         timer_flush(*t);
         if (t->open) cudaEventDestroy(t->open);
     }
