@@ -123,6 +123,89 @@ __global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* _
         if (s_hist[x]) atomicAdd(&hist[x], s_hist[x]);
 }
 
+// Level-1 prep (children are leaves): one warp per 32 consecutive parents. Their children
+// are a contiguous block of leaf rows, loaded with coalesced 8-byte words into shared memory;
+// each lane then reduces its own parent from shared memory, and the outputs are staged and
+// written back as contiguous words. Same arithmetic as k_lod_prep (exact integer sums).
+constexpr int PREP_WARPS = 4;
+
+template <int K>
+__global__ void __launch_bounds__(PREP_WARPS * 32)
+k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__ cacc,
+                const uint32_t* __restrict__ start, uint64_t V, uint64_t* __restrict__ pkey,
+                long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
+                uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+                uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
+    constexpr int MAXN = 8 * K;
+    extern __shared__ __align__(16) long long s_dyn[];   // per warp: rows | acc | lobes
+    __shared__ unsigned s_hist[MAXN + 1];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int x = threadIdx.x; x <= MAXN; x += blockDim.x) s_hist[x] = 0;
+    __syncthreads();
+    long long* rows = s_dyn + (size_t)wib * (256 * 7 + 32 * 7 + 32 * K * 7);
+    long long* sacc = rows + 256 * 7;
+    long long* slob = sacc + 32 * 7;
+    for (uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * 32; p0 < V;
+         p0 += (uint64_t)gridDim.x * PREP_WARPS * 32) {
+        const uint64_t pe = p0 + 32 < V ? p0 + 32 : V;
+        const int np = (int)(pe - p0);
+        const uint32_t cs = start[p0], ce = start[pe];
+        const int nw = (int)(ce - cs) * 7;
+        for (int w = lane; w < nw; w += 32) rows[w] = cacc[7 * (uint64_t)cs + w];
+        __syncwarp();
+        bool hard = false;
+        if (lane < np) {
+            const uint64_t p = p0 + lane;
+            const int c0 = (int)(start[p] - cs), c1 = (int)(start[p + 1] - cs);
+            long long sum[7] = {0, 0, 0, 0, 0, 0, 0};
+            int n = 0;
+            for (int x = c0; x < c1; x++) {
+#pragma unroll
+                for (int e = 0; e < 7; e++) sum[e] += rows[7 * x + e];
+                n += rows[7 * x] > 0;
+            }
+            pkey[p] = ckey[cs + c0] >> 3;
+#pragma unroll
+            for (int e = 0; e < 7; e++) sacc[7 * lane + e] = sum[e];
+            nlob[p] = (uint8_t)n;
+            hard = n > K;
+            int slot = 0;
+            for (int x = c0; x < c1 && slot < K; x++) {
+                if (rows[7 * x] > 0) {
+#pragma unroll
+                    for (int e = 0; e < 7; e++) slob[(lane * K + slot) * 7 + e] = rows[7 * x + e];
+                    slot++;
+                }
+            }
+            for (int q = slot; q < K; q++)
+#pragma unroll
+                for (int e = 0; e < 7; e++) slob[(lane * K + q) * 7 + e] = 0;
+            if (!hard) pncl[p] = (uint8_t)slot;
+            else atomicAdd(&s_hist[n], 1u);
+        }
+        const unsigned hmask = __ballot_sync(0xffffffffu, hard);
+        __syncwarp();
+        // coalesced write-back: accumulators, fp32 mass / m6, lobes of the final (n <= K) parents
+        for (int w = lane; w < np * 7; w += 32) {
+            const long long a = sacc[w];
+            pacc[7 * p0 + w] = a;
+            const int e = w % 7, pl = w / 7;
+            if (e == 0) pmass[p0 + pl] = deq32(a);
+            else pm6[6 * (p0 + pl) + e - 1] = deq32(a);
+        }
+        for (int w = lane; w < np * K * 7; w += 32) {
+            if ((hmask >> (w / (K * 7))) & 1u) continue;
+            const long long a = slob[w];
+            pclacc[(uint64_t)p0 * K * 7 + w] = a;
+            pcl[(uint64_t)p0 * K * 7 + w] = deq32(a);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x <= MAXN; x += blockDim.x)
+        if (s_hist[x]) atomicAdd(&hist[x], s_hist[x]);
+}
+
 // Exclusive offsets of the per-n buckets (ascending n) and the split between the quad
 // kernel (n <= 8) and the warp kernel (n > 8). counts = {n_small, n_total}.
 __global__ void k_bucket_init(const unsigned* __restrict__ hist, int K, int maxn, unsigned* __restrict__ cursor,
@@ -247,11 +330,9 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     long long(*lobe)[7] = s_lobe[wib][g];
     float(*Sg)[6] = s_S[wib][g];
     float* D = s_D[wib][g];
-    float cf[4][6];
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int e = 0; e < 6; e++) cf[q][e] = c_coef[l + 8 * q][e];
+    __shared__ float s_cf[32][6];
+    for (int x = threadIdx.x; x < 32 * 6; x += blockDim.x) s_cf[x / 6][x % 6] = c_coef[x / 6][x % 6];
+    __syncthreads();
     const unsigned small = counts[0];
     const unsigned nquad = (small + 3) / 4;
     for (unsigned qd = blockIdx.x * QUAD_WARPS + wib; qd < nquad; qd += gridDim.x * QUAD_WARPS) {
@@ -266,13 +347,18 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 c0 = start[p];
                 nch = (int)(start[p + 1] - c0);
             }
-            const bool has = l < nch && cacc[7 * (uint64_t)(c0 + l)] > 0;
+            long long a[7] = {0, 0, 0, 0, 0, 0, 0};
+            if (l < nch) {
+#pragma unroll
+                for (int e = 0; e < 7; e++) a[e] = cacc[7 * (uint64_t)(c0 + l) + e];
+            }
+            const bool has = l < nch && a[0] > 0;
             const unsigned gm = (__ballot_sync(0xffffffffu, has) >> (8 * g)) & 0xffu;
             n = __popc(gm);
             if (has) {
                 const int c = __popc(gm & ((1u << l) - 1u));
 #pragma unroll
-                for (int e = 0; e < 7; e++) lobe[c][e] = cacc[7 * (uint64_t)(c0 + l) + e];
+                for (int e = 0; e < 7; e++) lobe[c][e] = a[e];
             }
         } else {
             // 8 lanes x (child, lobe slot) rounds; n <= 8 here
@@ -312,17 +398,21 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         __syncwarp();
         float sg[8][4];
 #pragma unroll
-        for (int c = 0; c < 8; c++)
+        for (int q = 0; q < 4; q++) {
+            float cq[6];
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
+            for (int e = 0; e < 6; e++) cq[e] = s_cf[l + 8 * q][e];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
                 float qq = 0.0f;
                 if (c < nmax && valid && c < n) {
-                    qq = cf[q][0] * Sg[c][0];
+                    qq = cq[0] * Sg[c][0];
 #pragma unroll
-                    for (int e = 1; e < 6; e++) qq = qq + cf[q][e] * Sg[c][e];
+                    for (int e = 1; e < 6; e++) qq = qq + cq[e] * Sg[c][e];
                 }
                 sg[c][q] = (c < nmax) ? sqrtf(pmax(qq, 0.0f)) : 0.0f;
             }
+        }
 #pragma unroll
         for (int j = 1; j < 8; j++) {
             if (j >= nmax) break;
@@ -358,9 +448,9 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             for (int q = 0; q < 4; q++) {
                 float qq = 0.0f;
                 if (act) {
-                    qq = cf[q][0] * Sg[bi][0];
+                    qq = s_cf[l + 8 * q][0] * Sg[bi][0];
 #pragma unroll
-                    for (int e = 1; e < 6; e++) qq = qq + cf[q][e] * Sg[bi][e];
+                    for (int e = 1; e < 6; e++) qq = qq + s_cf[l + 8 * q][e] * Sg[bi][e];
                 }
                 sn[q] = sqrtf(pmax(qq, 0.0f));
             }
@@ -468,7 +558,6 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     float cf[6];
 #pragma unroll
     for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
-    const int l8 = lane & 7, g4 = lane >> 3;
     const unsigned lo = counts[0], hi = counts[1];
     for (unsigned w = lo + blockIdx.x * LOD_WARPS + wib; w < hi; w += gridDim.x * LOD_WARPS) {
         const uint64_t p = list[w];
@@ -537,18 +626,27 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 sig[bi][lane] = sqrtf(pmax(q, 0.0f));
             }
             __syncwarp();
-            // new row d(bi, x): 8 lanes per pair (lane l sums slices l, l+8, l+16, l+24 in the
-            // first two tree levels), then the last three levels by xor-shuffles in the group
-            for (int x0 = 0; x0 < n; x0 += 4) {
-                const int x = x0 + g4;
-                const int xr = x < n ? x : bi;
-                float s0 = fabsf(sig[bi][l8] - sig[xr][l8]) + fabsf(sig[bi][l8 + 16] - sig[xr][l8 + 16]);
-                float s1 = fabsf(sig[bi][l8 + 8] - sig[xr][l8 + 8]) + fabsf(sig[bi][l8 + 24] - sig[xr][l8 + 24]);
-                const float s = group_sum8(s0 + s1);
-                if (l8 == 0 && x < n && x != bi && ((alive >> x) & 1ull)) {
-                    const int a = x < bi ? x : bi, b2 = x < bi ? bi : x;
-                    D[pair_t(a, b2)] = ((unsigned long long)__float_as_uint(s) << 32) | (unsigned)((a << 8) | b2);
+            // new row d(bi, x): one pair per lane, the pinned tree in registers from two
+            // float4-read sigma rows (the merged row is a broadcast read)
+            for (int x = lane; x < n; x += 32) {
+                if (x == bi || !((alive >> x) & 1ull)) continue;
+                const float4* ri = reinterpret_cast<const float4*>(sig[bi]);
+                const float4* rx = reinterpret_cast<const float4*>(sig[x]);
+                float sv[32];
+#pragma unroll
+                for (int k4 = 0; k4 < 8; k4++) {
+                    const float4 u = ri[k4], w = rx[k4];
+                    sv[4 * k4 + 0] = fabsf(u.x - w.x);
+                    sv[4 * k4 + 1] = fabsf(u.y - w.y);
+                    sv[4 * k4 + 2] = fabsf(u.z - w.z);
+                    sv[4 * k4 + 3] = fabsf(u.w - w.w);
                 }
+#pragma unroll
+                for (int h = 16; h >= 1; h >>= 1)
+#pragma unroll
+                    for (int q = 0; q < h; q++) sv[q] = sv[q] + sv[q + h];
+                const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(sv[0]) << 32) | (unsigned)((a2 << 8) | b2);
             }
             // retire every pair of bj
             for (int x = lane; x < n; x += 32)
@@ -641,8 +739,18 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     CK(dalloc(c, (void**)&list, V * 4));
     CK(cudaMemsetAsync(hist, 0, 4 * (MAXN + 1), c->stream));
     timer_begin(c, c->t_prep);
-    k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, leaf, start, V, P.key, P.acc,
-                                                     P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
+    if (leaf) {
+        uint64_t pb = ((V + 31) / 32 + PREP_WARPS - 1) / PREP_WARPS;
+        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 16);
+        const size_t psm = (size_t)PREP_WARPS * (256 * 7 + 32 * 7 + 32 * K * 7) * sizeof(long long);
+        CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.key, C.acc, start, V, P.key, P.acc,
+                                                                            P.mass, P.m6, P.ncl, P.clacc, P.cl,
+                                                                            nlob, hist);
+    } else {
+        k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, leaf, start, V, P.key,
+                                                         P.acc, P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
+    }
     timer_end(c, c->t_prep);
     k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts);
     const uint64_t sb = (V + 256ull * SCATTER_PER_THREAD - 1) / (256ull * SCATTER_PER_THREAD);
