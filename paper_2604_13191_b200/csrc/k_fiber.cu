@@ -193,24 +193,6 @@ __device__ __forceinline__ bool far_from_capsule(const Fib& f, const float* d, f
 // ---------------------------------------------------------------- emit
 
 constexpr int EMIT_WARPS = 8;
-constexpr int EMIT_STAGE = 128;
-
-// Writes a warp's staged pairs to the global pair stream with one cursor atomic; returns 0.
-__device__ __forceinline__ int flush_stage(const uint64_t* qk, const uint64_t* qv, int qn, int lane,
-                                           uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, uint64_t cap,
-                                           unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)qn);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (int x = lane; x < qn; x += 32) {
-        const uint64_t pos = base + x;
-        if (pos < cap) { keys[pos] = qk[x]; vals[pos] = qv[x]; }
-        else atomicOr(flags, VOX_EFLAG_OVERFLOW);
-    }
-    __syncwarp();
-    return 0;
-}
-
 // One warp per batch of 32 consecutive segments. The batch's candidate voxels (the
 // unclamped AABB ranges, §3) are flattened and dealt round-robin to the 32 lanes, so every
 // lane evaluates one (segment, voxel) candidate per step whatever the segment sizes.
@@ -218,17 +200,13 @@ __device__ __forceinline__ int flush_stage(const uint64_t* qk, const uint64_t* q
 // compacted with a warp ballot and appended to the pair stream with one atomic per warp step.
 __global__ void __launch_bounds__(EMIT_WARPS * 32, 3)
 k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g, Shard sh,
-             uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab, uint64_t cap,
-             unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
+             Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab,
+             unsigned* __restrict__ flags) {
     __shared__ float s_f[EMIT_WARPS][16][32];
     __shared__ int64_t s_u0[EMIT_WARPS][3][32];
     __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
     __shared__ uint32_t s_start[EMIT_WARPS][32];
     __shared__ unsigned long long s_acc[EMIT_WARPS][32];
-    // per-warp staging of emitted pairs: one global cursor atomic per ~96-128 pairs instead of
-    // one per 32 candidates (a single hot counter serialises in L2), and coalesced writes
-    __shared__ uint64_t s_qk[EMIT_WARPS][EMIT_STAGE], s_qv[EMIT_WARPS][EMIT_STAGE];
-    int qn = 0;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nbatch = (S + 31) / 32;
     const float PI_F = 3.14159274101257324f;   // 0x40490FDB
@@ -335,15 +313,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             }
             const int onext = __shfl_down_sync(0xffffffffu, o, 1);
             if (o < 32 && (lane == 31 || onext != o)) s_acc[wib][o] += (unsigned long long)qv;
-            const unsigned bal = __ballot_sync(0xffffffffu, emit);
-            if (emit) {
-                const int pos = qn + __popc(bal & ((1u << lane) - 1u));
-                s_qk[wib][pos] = mkey;
-                s_qv[wib][pos] = val;
-            }
-            qn += __popc(bal);
-            __syncwarp();
-            if (qn > EMIT_STAGE - 32) qn = flush_stage(s_qk[wib], s_qv[wib], qn, lane, keys, vals, cap, cursor, flags);
+            if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
         }
         __syncwarp();
         if (p < S) {
@@ -363,26 +333,25 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
         }
         __syncwarp();
     }
-    if (qn) flush_stage(s_qk[wib], s_qv[wib], qn, lane, keys, vals, cap, cursor, flags);
 }
 
 cudaError_t launch_fiber_bound(vox_ctx* c, const float* seg, const float* rad, uint64_t S,
-                               unsigned long long* cellW, int T) {
+                               unsigned long long* cellW, int cell_log2) {
     const int threads = 256;
     uint64_t blocks = (S + threads - 1) / threads;
     if (blocks > 148ull * 64) blocks = 148ull * 64;
-    k_fiber_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(seg, rad, S, c->g, c->g.logN - T, cellW, c->d_flags);
+    k_fiber_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(seg, rad, S, c->g, cell_log2, cellW, c->d_flags);
     c->st.launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh,
-                              uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap) {
+cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh, Bins bins,
+                              uint64_t* keys, uint64_t* vals, float4* ptab) {
     const uint64_t nbatch = (S + 31) / 32;
     uint64_t blocks = (nbatch + EMIT_WARPS - 1) / EMIT_WARPS;
     if (blocks > (1ull << 30)) blocks = 1ull << 30;
-    k_fiber_emit<<<(unsigned)blocks, EMIT_WARPS * 32, 0, c->stream>>>(seg, rad, S, c->g, sh, keys, vals, ptab, cap,
-                                                                      c->d_counter, c->d_flags);
+    k_fiber_emit<<<(unsigned)blocks, EMIT_WARPS * 32, 0, c->stream>>>(seg, rad, S, c->g, sh, bins, keys, vals, ptab,
+                                                                      c->d_flags);
     c->st.launches++;
     return cudaGetLastError();
 }

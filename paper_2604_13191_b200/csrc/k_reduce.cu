@@ -3,8 +3,9 @@
 // pairs followed by a segmented reduction into exact fixed-point accumulators
 // (docs/PREDICATES.md §8). Also merges a new leaf set into an existing one (D19).
 //
-// Round-1 scaffold: the sort and the two scans use CUB (header-only, CUDA 12.9); the
-// per-voxel accumulation is ours. To be replaced by a fused bucket-sort + reduce kernel.
+// The per-call path is the binned reduce below (no sort). CUB (header-only, CUDA 12.9) is
+// used for exclusive scans and, only when a second voxelize call is merged into an existing
+// leaf set, for the merge sort.
 #include <cub/cub.cuh>
 
 #include "vox_internal.cuh"
@@ -22,33 +23,6 @@ __global__ void k_starts(const uint32_t* __restrict__ flags, const uint32_t* __r
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         if (flags[i]) start[incl[i] - 1] = (uint32_t)i;
         if (i == n - 1) start[incl[i]] = (uint32_t)n;
-    }
-}
-
-// One thread per voxel: exact sum of q(contribution) over its run of pairs (§5, §7, §8).
-__global__ void k_accum(const uint32_t* __restrict__ start, uint64_t V, const uint64_t* __restrict__ keys,
-                        const uint64_t* __restrict__ vals, const float4* __restrict__ ptab,
-                        uint64_t* __restrict__ okey, long long* __restrict__ oacc) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = start[v], e = start[v + 1];
-        long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0;
-        for (uint32_t i = s; i < e; i++) {
-            const uint64_t val = vals[i];
-            const float4 pt = ptab[(uint32_t)val];
-            const float w = __uint_as_float((uint32_t)(val >> 32));
-            const float mass = pt.w * w;
-            const float mx = mass * pt.x, my = mass * pt.y, mz = mass * pt.z;
-            a0 += q32(mass);
-            a1 += q32(mx * pt.x);
-            a2 += q32(my * pt.y);
-            a3 += q32(mz * pt.z);
-            a4 += q32(mx * pt.y);
-            a5 += q32(mx * pt.z);
-            a6 += q32(my * pt.z);
-        }
-        okey[v] = keys[s];
-        long long* o = oacc + 7 * v;
-        o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3; o[4] = a4; o[5] = a5; o[6] = a6;
     }
 }
 
@@ -119,13 +93,17 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     return VOX_OK;
 }
 
-static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t V) {
+static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6,
+                                  uint64_t V) {
     Level& L0 = c->lv[0];
     if (L0.n == 0) {
         free_level(c, L0);
         L0.n = V;
         L0.key = nkey;
         L0.acc = nacc;
+        L0.mass = nmass;
+        L0.m6 = nm6;
+        return VOX_OK;
     } else {
         timer_begin(c, c->t_merge);
         const uint64_t n0 = L0.n, tot = n0 + V;
@@ -163,6 +141,8 @@ static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, u
         dfree(c, k0); dfree(c, k1); dfree(c, i0); dfree(c, i1);
         dfree(c, nkey);
         dfree(c, nacc);
+        dfree(c, nmass);
+        dfree(c, nm6);
         free_level(c, L0);
         L0.n = VM;
         L0.key = mkey;
@@ -175,34 +155,356 @@ static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, u
     return VOX_OK;
 }
 
-vox_status reduce_pairs(vox_ctx* c, uint64_t* keys, uint64_t* keys_alt, uint64_t* vals, uint64_t* vals_alt,
-                        uint64_t P, const float4* ptab) {
-    if (P == 0) return VOX_OK;
-    timer_begin(c, c->t_sort);
-    cub::DoubleBuffer<uint64_t> dk(keys, keys_alt), dv(vals, vals_alt);
+// ---------------------------------------------------------------- binned reduce
+// Pairs were appended per bin (a Morton cell of 2^Lb voxels per edge, Lb <= 5, so a bin has at
+// most 32768 voxels). Within a bin, the set of distinct keys is a bitmap over the bin's local
+// Morton codes, and the position of a key in sorted order is the number of set bits below it
+// (word prefix + popc), so the "sort" of P:242-248 becomes an O(1) rank per pair. Pass 1 counts
+// distinct keys per bin; an exclusive scan gives every bin's first output slot; pass 2 sums the
+// exact fixed-point contributions (§5, §7, §8) of each key in shared memory by rank and writes
+// the bin's voxels contiguously in key order.
+
+__global__ void k_group_sum(const unsigned long long* __restrict__ Wb, uint64_t nT, uint64_t group,
+                            unsigned long long* __restrict__ WT) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nT; c += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long s = 0;
+        for (uint64_t x = 0; x < group; x++) s += Wb[c * group + x];
+        WT[c] = s;
+    }
+}
+
+__global__ void k_bin_caps(const unsigned long long* __restrict__ Wb, uint64_t nb, int gshift, uint64_t lo,
+                           uint64_t hi, unsigned long long* __restrict__ caps) {
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= nb; b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t top = b >> gshift;
+        caps[b] = (b < nb && top >= lo && top < hi) ? Wb[b] : 0ull;
+    }
+}
+
+constexpr int BIN_THREADS = 256;
+
+// Compact list of the non-empty bins (order irrelevant: every bin writes its own slots).
+__global__ void k_bin_active(const unsigned* __restrict__ cnt, uint64_t nb, unsigned* __restrict__ list,
+                             unsigned* __restrict__ nact) {
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb; b += (uint64_t)gridDim.x * blockDim.x) {
+        const bool act = cnt[b] != 0;
+        const unsigned m = __ballot_sync(__activemask(), act);
+        if (!m) continue;
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(nact, (unsigned)__popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (act) list[base + __popc(m & ((1u << lane) - 1u))] = (unsigned)b;
+    }
+}
+
+// pass 1: distinct keys per bin (bitmap popcount); also totals the pairs
+__global__ void __launch_bounds__(BIN_THREADS)
+k_bin_count(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ off,
+            const unsigned* __restrict__ cnt, const unsigned* __restrict__ alist, const unsigned* __restrict__ nact,
+            int lbits, unsigned* __restrict__ vcount, unsigned long long* __restrict__ npairs) {
+    extern __shared__ unsigned s_bm[];
+    __shared__ unsigned s_red[BIN_THREADS / 32];
+    const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
+    const uint64_t lmask = (1ull << lbits) - 1ull;
+    const unsigned na = *nact;
+    for (unsigned ai = blockIdx.x; ai < na; ai += gridDim.x) {
+        const unsigned b = alist[ai];
+        const unsigned n = cnt[b];
+        for (int w = threadIdx.x; w < words; w += blockDim.x) s_bm[w] = 0u;
+        __syncthreads();
+        const uint64_t o = off[b];
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned lk = (unsigned)(keys[o + i] & lmask);
+            atomicOr(&s_bm[lk >> 5], 1u << (lk & 31));
+        }
+        __syncthreads();
+        unsigned c = 0;
+        for (int w = threadIdx.x; w < words; w += blockDim.x) c += __popc(s_bm[w]);
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned t = 0;
+            for (int q = 0; q < BIN_THREADS / 32; q++) t += s_red[q];
+            vcount[b] = t;
+            atomicAdd(npairs, (unsigned long long)n);
+        }
+        __syncthreads();
+    }
+}
+
+constexpr int BIN_NMAX = 16384;   // pairs of a bin handled by the in-shared-memory counting sort
+constexpr int BIN_VMAX = 12288;   // distinct keys of such a bin
+constexpr int BIN_CHUNK = 1024;   // voxels per pass of the fallback path (larger bins)
+
+// exclusive prefix of popcounts of the bitmap words (block scan over <= 1024 words)
+__device__ __forceinline__ void bitmap_prefix(const unsigned* bm, unsigned* wpre, int words, unsigned* s_wsum) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int per = (words + BIN_THREADS - 1) / BIN_THREADS;
+    const int w0 = threadIdx.x * per;
+    unsigned loc = 0;
+    for (int q = 0; q < per; q++)
+        if (w0 + q < words) loc += __popc(bm[w0 + q]);
+    unsigned inc = loc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) s_wsum[wid] = inc;
+    __syncthreads();
+    unsigned run = inc - loc;
+    for (int q = 0; q < wid; q++) run += s_wsum[q];
+    for (int q = 0; q < per; q++)
+        if (w0 + q < words) {
+            wpre[w0 + q] = run;
+            run += __popc(bm[w0 + q]);
+        }
+    __syncthreads();
+}
+
+__device__ __forceinline__ unsigned key_rank(const unsigned* bm, const unsigned* wpre, unsigned lk) {
+    const unsigned w = lk >> 5, bit = lk & 31;
+    return wpre[w] + __popc(bm[w] & ((1u << bit) - 1u));
+}
+
+// one voxel's exact sums over its pairs (§5, §7, §8), written as a key-ordered output row
+__device__ __forceinline__ void emit_voxel(uint64_t key, const long long (&a)[7], uint64_t r, uint64_t* okey,
+                                          long long* oacc, float* omass, float* om6) {
+    okey[r] = key;
+#pragma unroll
+    for (int e = 0; e < 7; e++) oacc[7 * r + e] = a[e];
+    omass[r] = deq32(a[0]);
+#pragma unroll
+    for (int e = 0; e < 6; e++) om6[6 * r + e] = deq32(a[1 + e]);
+}
+
+__device__ __forceinline__ void add_pair(uint64_t val, const float4* __restrict__ ptab, long long (&a)[7]) {
+    const float4 pt = ptab[(uint32_t)val];
+    const float wgt = __uint_as_float((uint32_t)(val >> 32));
+    const float mass = pt.w * wgt;
+    const float mx = mass * pt.x, my = mass * pt.y, mz = mass * pt.z;
+    a[0] += q32(mass);
+    a[1] += q32(mx * pt.x);
+    a[2] += q32(my * pt.y);
+    a[3] += q32(mz * pt.z);
+    a[4] += q32(mx * pt.y);
+    a[5] += q32(mx * pt.z);
+    a[6] += q32(my * pt.z);
+}
+
+// pass 2: per bin, ranks from the bitmap; bins of <= BIN_NMAX pairs and <= BIN_VMAX keys are
+// counting-sorted by rank in shared memory and each thread then sums whole voxels in
+// registers (no 64-bit atomics); larger bins take the chunked path with shared atomics.
+__global__ void __launch_bounds__(BIN_THREADS)
+k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, const float4* __restrict__ ptab,
+             const unsigned long long* __restrict__ off, const unsigned* __restrict__ cnt,
+             const unsigned* __restrict__ alist, const unsigned* __restrict__ nact,
+             const unsigned* __restrict__ voff, int lbits, uint64_t* __restrict__ okey,
+             long long* __restrict__ oacc, float* __restrict__ omass, float* __restrict__ om6) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
+    unsigned* bm = reinterpret_cast<unsigned*>(s_raw);                      // [words]
+    unsigned* wpre = bm + 1024;                                             // [words]
+    unsigned* cur = wpre + 1024;                                            // [BIN_VMAX + 1]
+    unsigned short* sidx = reinterpret_cast<unsigned short*>(cur + BIN_VMAX + 1);   // [BIN_NMAX]
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(cur);   // fallback: [BIN_CHUNK][7]
+    unsigned short* lkey = reinterpret_cast<unsigned short*>(acc + BIN_CHUNK * 7);   // fallback: [BIN_CHUNK]
+    __shared__ unsigned s_wsum[BIN_THREADS / 32];
+    const uint64_t lmask = (1ull << lbits) - 1ull;
+    const unsigned na = *nact;
+    for (unsigned ai = blockIdx.x; ai < na; ai += gridDim.x) {
+        const unsigned b = alist[ai];
+        const unsigned n = cnt[b];
+        const uint64_t o = off[b];
+        const unsigned vb = voff[b], V = voff[b + 1] - vb;
+        const uint64_t kbase = (uint64_t)b << lbits;
+        for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned lk = (unsigned)(keys[o + i] & lmask);
+            atomicOr(&bm[lk >> 5], 1u << (lk & 31));
+        }
+        __syncthreads();
+        bitmap_prefix(bm, wpre, words, s_wsum);
+        if (n <= BIN_NMAX && V <= BIN_VMAX) {
+            for (unsigned r = threadIdx.x; r <= V; r += blockDim.x) cur[r] = 0u;
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+                atomicAdd(&cur[key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask)) + 1], 1u);
+            __syncthreads();
+            // inclusive scan of cur[1..V] -> cur[r] = first slot of rank r (cur[0] = 0)
+            {
+                const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                const unsigned per = (V + 1 + BIN_THREADS - 1) / BIN_THREADS;
+                const unsigned r0 = threadIdx.x * per;
+                unsigned loc = 0;
+                for (unsigned q = 0; q < per; q++)
+                    if (r0 + q <= V) loc += cur[r0 + q];
+                unsigned inc = loc;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += y;
+                }
+                if (lane == 31) s_wsum[wid] = inc;
+                __syncthreads();
+                unsigned run = inc - loc;
+                for (int q = 0; q < wid; q++) run += s_wsum[q];
+                for (unsigned q = 0; q < per; q++)
+                    if (r0 + q <= V) {
+                        run += cur[r0 + q];
+                        cur[r0 + q] = run;
+                    }
+                __syncthreads();
+            }
+            // scatter pair indices by rank; afterwards cur[r] = end of rank r's run
+            for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+                const unsigned r = key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask));
+                sidx[atomicAdd(&cur[r], 1u)] = (unsigned short)i;
+            }
+            __syncthreads();
+            for (unsigned r = threadIdx.x; r < V; r += blockDim.x) {
+                const unsigned p0 = r == 0 ? 0u : cur[r - 1], p1 = cur[r];
+                long long a[7] = {0, 0, 0, 0, 0, 0, 0};
+                for (unsigned p = p0; p < p1; p++) add_pair(vals[o + sidx[p]], ptab, a);
+                emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc, omass, om6);
+            }
+            __syncthreads();
+        } else {
+            for (unsigned r0 = 0; r0 < V; r0 += BIN_CHUNK) {
+                const unsigned rn = V - r0 < BIN_CHUNK ? V - r0 : BIN_CHUNK;
+                for (unsigned x = threadIdx.x; x < rn * 7; x += blockDim.x) acc[x] = 0ull;
+                for (int w = threadIdx.x; w < words; w += blockDim.x) {
+                    unsigned m = bm[w];
+                    unsigned r = wpre[w];
+                    while (m) {
+                        const int bit = __ffs(m) - 1;
+                        m &= m - 1;
+                        if (r >= r0 && r < r0 + rn) lkey[r - r0] = (unsigned short)((w << 5) | bit);
+                        r++;
+                    }
+                }
+                __syncthreads();
+                for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+                    const unsigned r = key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask));
+                    if (r < r0 || r >= r0 + rn) continue;
+                    long long a[7] = {0, 0, 0, 0, 0, 0, 0};
+                    add_pair(vals[o + i], ptab, a);
+                    unsigned long long* d = acc + 7 * (r - r0);
+#pragma unroll
+                    for (int e = 0; e < 7; e++) atomicAdd(d + e, (unsigned long long)a[e]);
+                }
+                __syncthreads();
+                for (unsigned x = threadIdx.x; x < rn; x += blockDim.x) {
+                    long long a[7];
+#pragma unroll
+                    for (int e = 0; e < 7; e++) a[e] = (long long)acc[7 * x + e];
+                    emit_voxel(kbase | lkey[x], a, (uint64_t)vb + r0 + x, okey, oacc, omass, om6);
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// Top-cell candidate counts (sum of the bins of each top cell) for the shard plan.
+vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT) {
+    const uint64_t nT = 1ull << (3 * c->T);
+    const uint64_t group = 1ull << (3 * (c->g.logN - Lb - c->T));
+    unsigned long long* dWT = nullptr;
+    CK(dalloc(c, (void**)&dWT, nT * 8));
+    k_group_sum<<<grid_for(nT), 256, 0, c->stream>>>(Wb, nT, group, dWT);
+    c->st.launches++;
+    WT.resize(nT);
+    CK(cudaMemcpyAsync(WT.data(), dWT, nT * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, dWT);
+    return VOX_OK;
+}
+
+// Capacity offsets of the bins of this rank's top cells; *cap_out = total (one 8-byte read).
+vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigned long long** off_out,
+                       uint64_t* cap_out) {
+    const uint64_t nb = 1ull << (3 * (c->g.logN - Lb));
+    const int gshift = 3 * (c->g.logN - Lb - c->T);
+    unsigned long long *caps = nullptr, *off = nullptr;
     void* tmp = nullptr;
     size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int64_t)P, 0, 3 * c->g.logN, c->stream));
+    CK(dalloc(c, (void**)&caps, (nb + 1) * 8));
+    CK(dalloc(c, (void**)&off, (nb + 1) * 8));
+    k_bin_caps<<<grid_for(nb + 1), 256, 0, c->stream>>>(Wb, nb, gshift, c->cell_lo, c->cell_hi, caps);
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, caps, off, (int64_t)(nb + 1), c->stream));
     CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)P, 0, 3 * c->g.logN, c->stream));
-    c->st.launches += 2 + (3 * c->g.logN + 7) / 8;   // histogram + exclusive sum + one onesweep pass per 8 bits
-    timer_end(c, c->t_sort);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, caps, off, (int64_t)(nb + 1), c->stream));
+    c->st.launches += 3;
+    unsigned long long cap = 0;
+    CK(cudaMemcpyAsync(&cap, off + nb, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     dfree(c, tmp);
+    dfree(c, caps);
+    *off_out = off;
+    *cap_out = cap;
+    return VOX_OK;
+}
+
+vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, Bins bins, uint64_t nb,
+                       const float4* ptab) {
+    const int lbits = bins.shift;
+    const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
+    unsigned* vcount = nullptr;
+    unsigned* voff = nullptr;
+    unsigned long long* npairs = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    timer_begin(c, c->t_sort);
+    CK(dalloc(c, (void**)&vcount, (nb + 1) * 4));
+    CK(dalloc(c, (void**)&voff, (nb + 1) * 4));
+    CK(dalloc(c, (void**)&npairs, 16));
+    unsigned* alist = nullptr;
+    CK(dalloc(c, (void**)&alist, nb * 4));
+    unsigned* nact = reinterpret_cast<unsigned*>(npairs + 1);
+    CK(cudaMemsetAsync(npairs, 0, 16, c->stream));
+    CK(cudaMemsetAsync(vcount, 0, (nb + 1) * 4, c->stream));
+    k_bin_active<<<grid_for(nb), 256, 0, c->stream>>>(bins.cnt, nb, alist, nact);
+    const unsigned grid = (unsigned)std::min<uint64_t>(nb, 148ull * 8);
+    k_bin_count<<<grid, BIN_THREADS, words * 4, c->stream>>>(keys, bins.off, bins.cnt, alist, nact, lbits, vcount,
+                                                             npairs);
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, vcount, voff, (int64_t)(nb + 1), c->stream));
+    CK(dalloc(c, &tmp, tb));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, vcount, voff, (int64_t)(nb + 1), c->stream));
+    c->st.launches += 4;
+    unsigned V = 0;
+    unsigned long long P = 0;
+    CK(cudaMemcpyAsync(&V, voff + nb, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&P, npairs, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    timer_end(c, c->t_sort);
+    c->st.pairs = P;
     timer_begin(c, c->t_reduce);
-    uint32_t* start = nullptr;
-    uint64_t V = 0;
-    vox_status s = find_runs(c, dk.Current(), P, &start, &V);
-    if (s != VOX_OK) return s;
     uint64_t* nkey = nullptr;
     long long* nacc = nullptr;
-    CK(dalloc(c, (void**)&nkey, V * 8));
-    CK(dalloc(c, (void**)&nacc, V * 56));
-    k_accum<<<grid_for(V), 256, 0, c->stream>>>(start, V, dk.Current(), dv.Current(), ptab, nkey, nacc);
+    float *nmass = nullptr, *nm6 = nullptr;
+    CK(dalloc(c, (void**)&nkey, (uint64_t)V * 8));
+    CK(dalloc(c, (void**)&nacc, (uint64_t)V * 56));
+    CK(dalloc(c, (void**)&nmass, (uint64_t)V * 4));
+    CK(dalloc(c, (void**)&nm6, (uint64_t)V * 24));
+    const size_t smem = 2 * 1024 * 4 + (BIN_VMAX + 1) * 4 + BIN_NMAX * 2 + 16;
+    static_assert(BIN_CHUNK * 7 * 8 + BIN_CHUNK * 2 <= (BIN_VMAX + 1) * 4 + BIN_NMAX * 2, "fallback must fit");
+    CK(cudaFuncSetAttribute(k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bin_reduce<<<grid, BIN_THREADS, smem, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact, voff,
+                                                         lbits, nkey, nacc, nmass, nm6);
     c->st.launches++;
-    dfree(c, start);
+    CK(cudaGetLastError());
     timer_end(c, c->t_reduce);
+    dfree(c, tmp);
+    dfree(c, vcount);
+    dfree(c, voff);
+    dfree(c, npairs);
+    dfree(c, alist);
     c->st.voxels = V;
-    return merge_into_leaf(c, nkey, nacc, V);
+    return merge_into_leaf(c, nkey, nacc, nmass, nm6, V);
 }
 
 }  // namespace vox

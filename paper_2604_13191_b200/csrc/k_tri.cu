@@ -202,8 +202,8 @@ constexpr int TRI_WARPS = 4;
 // (key, prim | area) pairs; the prim table holds (d_hat, f = 1).
 __global__ void __launch_bounds__(TRI_WARPS * 32)
 k_tri_emit(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx, Shard sh,
-           uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab, uint64_t cap,
-           unsigned long long* __restrict__ cursor, unsigned* __restrict__ flags) {
+           Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab,
+           unsigned* __restrict__ flags) {
     __shared__ float s_g[TRI_WARPS][9][32];
     __shared__ int64_t s_e0[TRI_WARPS][3][32];
     __shared__ uint32_t s_ex[TRI_WARPS][2][32];
@@ -266,40 +266,29 @@ k_tri_emit(const float* __restrict__ tri, const float* __restrict__ dirs, uint64
                     }
                 }
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, emit);
-            if (bal) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(cursor, (unsigned long long)__popc(bal));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (emit) {
-                    const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
-                    if (pos < cap) { keys[pos] = mkey; vals[pos] = val; }
-                    else atomicOr(flags, VOX_EFLAG_OVERFLOW);
-                }
-            }
+            if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
         }
         __syncwarp();
     }
 }
 
 cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, unsigned long long* cellW,
-                             int Tdepth) {
+                             int cell_log2) {
     const int threads = 256;
     uint64_t blocks = (T + threads - 1) / threads;
     if (blocks > 148ull * 64) blocks = 148ull * 64;
-    k_tri_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(tri, dirs, T, c->g, c->g.logN - Tdepth, cellW,
-                                                             c->d_flags);
+    k_tri_bound<<<(unsigned)blocks, threads, 0, c->stream>>>(tri, dirs, T, c->g, cell_log2, cellW, c->d_flags);
     c->st.launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, uint64_t* keys,
-                            uint64_t* vals, float4* ptab, uint64_t cap) {
+cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, Bins bins,
+                            uint64_t* keys, uint64_t* vals, float4* ptab) {
     const uint64_t nbatch = (T + 31) / 32;
     uint64_t blocks = (nbatch + TRI_WARPS - 1) / TRI_WARPS;
     if (blocks > (1ull << 30)) blocks = 1ull << 30;
-    k_tri_emit<<<(unsigned)blocks, TRI_WARPS * 32, 0, c->stream>>>(tri, dirs, T, c->g, sh, keys, vals, ptab, cap,
-                                                                   c->d_counter, c->d_flags);
+    k_tri_emit<<<(unsigned)blocks, TRI_WARPS * 32, 0, c->stream>>>(tri, dirs, T, c->g, sh, bins, keys, vals, ptab,
+                                                                   c->d_flags);
     c->st.launches++;
     return cudaGetLastError();
 }

@@ -165,31 +165,37 @@ vox_status vox_plan_shards(const uint64_t* w, uint64_t ncells, int world, uint64
 }
 
 // Common tail of the two voxelize entry points: bound (done), plan, capacity, emit, reduce.
-typedef cudaError_t (*emit_fn)(vox_ctx*, const float*, const float*, uint64_t, Shard, uint64_t*, uint64_t*,
-                               float4*, uint64_t);
+typedef cudaError_t (*emit_fn)(vox_ctx*, const float*, const float*, uint64_t, Shard, Bins, uint64_t*, uint64_t*,
+                               float4*);
 
-static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* cellW,
+static int bin_log2(const vox_ctx* c) { return std::min(5, c->g.logN - c->T); }
+static uint64_t nbins_of(const vox_ctx* c) { return 1ull << (3 * (c->g.logN - bin_log2(c))); }
+
+static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* Wb,
                                   emit_fn emit) {
-    const uint64_t ncells = ncells_of(c);
-    std::vector<uint64_t> W(ncells);
+    const uint64_t ncells = ncells_of(c), nb = nbins_of(c);
+    const int Lb = bin_log2(c);
     unsigned fl = 0;
-    CKS(cudaMemcpyAsync(W.data(), cellW, ncells * 8, cudaMemcpyDeviceToHost, c->stream));
     CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
     CKS(cudaStreamSynchronize(c->stream));
     timer_end(c, c->t_bound);
-    dfree(c, cellW);
     if (fl) {
+        dfree(c, Wb);
         c->err = std::string("invalid input:") + ((fl & VOX_EFLAG_NONFINITE) ? " non-finite value" : "") +
                  ((fl & VOX_EFLAG_NEG_RADIUS) ? " negative radius" : "") +
                  ((fl & VOX_EFLAG_TOO_MANY_CAND) ? " segment with more than 2^24 candidate voxels" : "") +
                  ((fl & VOX_EFLAG_ZERO_DIR) ? " zero-norm dir" : "");
         return VOX_ERR_INVALID_ARG;
     }
+    vox_status s;
     if (!c->plan_fixed) {
         if (c->world == 1) {
             c->cell_lo = 0;
             c->cell_hi = ncells;
         } else {
+            std::vector<uint64_t> W;
+            s = bin_topcells(c, Wb, Lb, W);
+            if (s != VOX_OK) return s;
             std::vector<uint64_t> bounds(c->world + 1);
             vox_plan_shards(W.data(), ncells, c->world, bounds.data());
             c->cell_lo = bounds[c->rank];
@@ -199,63 +205,74 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
         c->st.cell_lo = c->cell_lo;
         c->st.cell_hi = c->cell_hi;
     }
+    unsigned long long* off = nullptr;
     uint64_t cap = 0;
-    for (uint64_t x = c->cell_lo; x < c->cell_hi; x++) cap += W[x];
+    s = bin_offsets(c, Wb, Lb, &off, &cap);
+    dfree(c, Wb);
+    if (s != VOX_OK) return s;
     c->st.candidates = cap;
     c->st.pairs = 0;
     if (cap >= (1ull << 32)) {
+        dfree(c, off);
         c->err = "more than 2^32 candidate voxels in one call: split the primitives into batches";
         return VOX_ERR_CAPACITY;
     }
     if (cap == 0) {
+        dfree(c, off);
         c->state = ST_VOXELIZED;
         return VOX_OK;
     }
-    // estimate: pairs x2 (sort buffers) + sort temp + run scans + new leaf + ptab + merge
-    const uint64_t est = cap * 32 + cap * 16 + cap * 12 + cap * 64 + n * 16 + c->lv[0].n * 88;
+    // estimate: pairs + per-bin scans + new leaf (<= cap voxels) + prim table + merge
+    const uint64_t est = cap * 16 + nb * 24 + cap * 92 + n * 16 + c->lv[0].n * 92;
     if (c->max_bytes && est > c->max_bytes) {
+        dfree(c, off);
         c->err = "estimated " + std::to_string(est) + " bytes exceed max_bytes";
         return VOX_ERR_CAPACITY;
     }
     uint64_t *keys = nullptr, *vals = nullptr;
     float4* ptab = nullptr;
-    CKS(dalloc(c, (void**)&keys, cap * 16));
-    CKS(dalloc(c, (void**)&vals, cap * 16));
+    unsigned* bcnt = nullptr;
+    CKS(dalloc(c, (void**)&keys, cap * 8));
+    CKS(dalloc(c, (void**)&vals, cap * 8));
     CKS(dalloc(c, (void**)&ptab, n * sizeof(float4)));
-    CKS(cudaMemsetAsync(c->d_counter, 0, 8, c->stream));
+    CKS(dalloc(c, (void**)&bcnt, nb * 4));
+    CKS(cudaMemsetAsync(bcnt, 0, nb * 4, c->stream));
     Shard sh;
     sh.shift = 3 * (c->g.logN - c->T);
     sh.cell_lo = c->cell_lo;
     sh.cell_hi = c->cell_hi;
+    Bins bins;
+    bins.shift = 3 * Lb;
+    bins.off = off;
+    bins.cnt = bcnt;
     timer_begin(c, c->t_emit);
-    CKS(emit(c, a, b, n, sh, keys, vals, ptab, cap));
+    CKS(emit(c, a, b, n, sh, bins, keys, vals, ptab));
     timer_end(c, c->t_emit);
-    unsigned long long P = 0;
-    CKS(cudaMemcpyAsync(&P, c->d_counter, 8, cudaMemcpyDeviceToHost, c->stream));
+    s = reduce_bins(c, keys, vals, bins, nb, ptab);
     CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
     CKS(cudaStreamSynchronize(c->stream));
+    dfree(c, keys);
+    dfree(c, vals);
+    dfree(c, ptab);
+    dfree(c, bcnt);
+    dfree(c, off);
+    if (s != VOX_OK) return s;
     if (fl & VOX_EFLAG_OVERFLOW) {
         c->err = "internal: pair capacity overflow";
         return VOX_ERR_CUDA;
     }
-    c->st.pairs = P;
-    vox_status s = reduce_pairs(c, keys, keys + cap, vals, vals + cap, P, ptab);
-    dfree(c, keys);
-    dfree(c, vals);
-    dfree(c, ptab);
-    if (s != VOX_OK) return s;
     c->state = ST_VOXELIZED;
     return VOX_OK;
 }
 
-static cudaError_t emit_fibers(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh, uint64_t* keys,
-                               uint64_t* vals, float4* ptab, uint64_t cap) {
-    return launch_fiber_emit(c, seg, rad, S, sh, keys, vals, ptab, cap);
+static cudaError_t emit_fibers(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh, Bins bins,
+                               uint64_t* keys, uint64_t* vals, float4* ptab) {
+    return launch_fiber_emit(c, seg, rad, S, sh, bins, keys, vals, ptab);
 }
 
-static cudaError_t emit_tris(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, uint64_t* keys,
-                             uint64_t* vals, float4* ptab, uint64_t cap) {
-    return launch_tri_emit(c, tri, dirs, T, sh, keys, vals, ptab, cap);
+static cudaError_t emit_tris(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, Bins bins,
+                             uint64_t* keys, uint64_t* vals, float4* ptab) {
+    return launch_tri_emit(c, tri, dirs, T, sh, bins, keys, vals, ptab);
 }
 
 vox_status vox_voxelize_fibers(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
@@ -268,12 +285,12 @@ vox_status vox_voxelize_fibers(vox_ctx* c, const float* segments, const float* r
     c->st.segments = S;
     timer_begin(c, c->t_vox);
     timer_begin(c, c->t_bound);
-    const uint64_t ncells = ncells_of(c);
+    const uint64_t nb = nbins_of(c);
     unsigned long long* cellW = nullptr;
-    CKS(dalloc(c, (void**)&cellW, ncells * 8));
-    CKS(cudaMemsetAsync(cellW, 0, ncells * 8, c->stream));
+    CKS(dalloc(c, (void**)&cellW, nb * 8));
+    CKS(cudaMemsetAsync(cellW, 0, nb * 8, c->stream));
     CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
-    CKS(launch_fiber_bound(c, segments, radii, S, cellW, c->T));
+    CKS(launch_fiber_bound(c, segments, radii, S, cellW, bin_log2(c)));
     s = voxelize_common(c, segments, radii, S, cellW, emit_fibers);
     timer_end(c, c->t_vox);
     return s;
@@ -289,12 +306,12 @@ vox_status vox_voxelize_triangles(vox_ctx* c, const float* tris, const float* di
     c->st.segments = T;
     timer_begin(c, c->t_vox);
     timer_begin(c, c->t_bound);
-    const uint64_t ncells = ncells_of(c);
+    const uint64_t nb = nbins_of(c);
     unsigned long long* cellW = nullptr;
-    CKS(dalloc(c, (void**)&cellW, ncells * 8));
-    CKS(cudaMemsetAsync(cellW, 0, ncells * 8, c->stream));
+    CKS(dalloc(c, (void**)&cellW, nb * 8));
+    CKS(cudaMemsetAsync(cellW, 0, nb * 8, c->stream));
     CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
-    CKS(launch_tri_bound(c, tris, dirs, T, cellW, c->T));
+    CKS(launch_tri_bound(c, tris, dirs, T, cellW, bin_log2(c)));
     s = voxelize_common(c, tris, dirs, T, cellW, emit_tris);
     timer_end(c, c->t_vox);
     return s;

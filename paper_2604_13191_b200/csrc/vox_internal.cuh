@@ -83,6 +83,37 @@ struct Shard {
     uint64_t cell_lo, cell_hi;
 };
 
+// Pair bins: Morton cells of 2^Lb voxels per edge (bin id = key >> shift, shift = 3 Lb).
+// Each bin owns the pair slots [off[b], off[b+1]) -- its exact candidate count, an upper
+// bound on its keys -- and cnt[b] pairs are appended there by the emit kernels.
+struct Bins {
+    int shift;
+    const unsigned long long* off;   // [nb + 1]
+    unsigned* cnt;                   // [nb]
+};
+
+// Appends the emitting lanes' pairs to their bins: lanes with the same bin share one atomic
+// (warp match), and get consecutive slots. Must be called by the whole warp.
+__device__ __forceinline__ void append_binned(bool emit, uint64_t mkey, uint64_t val, int lane, const Bins& bins,
+                                              uint64_t* __restrict__ keys, uint64_t* __restrict__ vals,
+                                              unsigned* __restrict__ flags) {
+    const unsigned long long bk = emit ? (mkey >> bins.shift) : ~0ull;
+    const unsigned m = __match_any_sync(0xffffffffu, bk);
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (emit && lane == leader) base = bins.off[bk] + atomicAdd(&bins.cnt[bk], (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (emit) {
+        const uint64_t pos = base + __popc(m & ((1u << lane) - 1u));
+        if (pos < bins.off[bk + 1]) {
+            keys[pos] = mkey;
+            vals[pos] = val;
+        } else {
+            atomicOr(flags, VOX_EFLAG_OVERFLOW);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- host-side state
 
 struct Level {
@@ -142,17 +173,21 @@ void timer_end(vox_ctx* c, StageTimer& t);
 
 // fibers (k_fiber.cu)
 cudaError_t launch_fiber_bound(vox_ctx* c, const float* seg, const float* rad, uint64_t S,
-                               unsigned long long* cellW, int T);
-cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh,
-                              uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap);
+                               unsigned long long* cellW, int cell_log2);
+cudaError_t launch_fiber_emit(vox_ctx* c, const float* seg, const float* rad, uint64_t S, Shard sh, Bins bins,
+                              uint64_t* keys, uint64_t* vals, float4* ptab);
 // triangles (k_tri.cu)
 cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, unsigned long long* cellW,
-                             int Tdepth);
-cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh,
-                            uint64_t* keys, uint64_t* vals, float4* ptab, uint64_t cap);
-// sort + segmented reduce (k_reduce.cu): pairs -> new leaf set merged into lv[0]
-vox_status reduce_pairs(vox_ctx* c, uint64_t* keys, uint64_t* keys_alt, uint64_t* vals, uint64_t* vals_alt,
-                        uint64_t P, const float4* ptab);
+                             int cell_log2);
+cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, Bins bins,
+                            uint64_t* keys, uint64_t* vals, float4* ptab);
+// binned reduce (k_reduce.cu): per-bin pair lists -> new leaf set merged into lv[0]
+vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, Bins bins, uint64_t nb,
+                       const float4* ptab);
+// per-call helpers (k_reduce.cu)
+vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT);
+vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigned long long** off_out,
+                       uint64_t* cap_out);
 // LoD (k_lod.cu)
 vox_status build_level(vox_ctx* c, int l);
 void upload_theta(vox_ctx* c);
