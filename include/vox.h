@@ -81,6 +81,7 @@ typedef struct {
     /* SGGX-H algorithmic work since the last reset (profile=1): lobe sigma evaluations
      * (32 slices each), pair distance evaluations (32 slices each), parents with n > k */
     uint64_t lod_sigma_evals, lod_dist_evals, lod_hard_parents;
+    double host_ms_alloc, host_ms_sync;   /* host time in stream-ordered allocation / stream syncs */
 } vox_stats;
 
 /* Create a ctx for an N^3 grid over the cubic extent of bbox (D3).
@@ -151,6 +152,9 @@ vox_status vox_theta_table(float* theta, float* coef);
 
 vox_status vox_stats_get(vox_ctx* ctx, vox_stats* out);   /* synchronises the stream */
 vox_status vox_stats_reset(vox_ctx* ctx);
+/* Release the library's cached device blocks of the ctx stream (freed scratch and levels of
+ * destroyed ctxs are kept for reuse by later calls on the same stream). */
+vox_status vox_trim(vox_ctx* ctx);
 vox_status vox_sync(vox_ctx* ctx);
 const char* vox_status_str(vox_status s);
 const char* vox_last_error(vox_ctx* ctx);

@@ -50,7 +50,7 @@ class _Stats(C.Structure):
                 ("ms_lod", C.c_double), ("ms_total_vox", C.c_double), ("ms_total_lod", C.c_double),
                 ("ms_lod_prep", C.c_double), ("ms_sggxh_quad", C.c_double), ("ms_sggxh_warp", C.c_double),
                 ("launches", C.c_uint64), ("lod_sigma_evals", C.c_uint64), ("lod_dist_evals", C.c_uint64),
-                ("lod_hard_parents", C.c_uint64)]
+                ("lod_hard_parents", C.c_uint64), ("host_ms_alloc", C.c_double), ("host_ms_sync", C.c_double)]
 
 
 _lib = None
@@ -82,6 +82,7 @@ def lib():
     L.vox_stats_get.argtypes = [vp, C.POINTER(_Stats)]
     L.vox_stats_reset.argtypes = [vp]
     L.vox_sync.argtypes = [vp]
+    L.vox_trim.argtypes = [vp]
     L.vox_status_str.restype = C.c_char_p
     L.vox_status_str.argtypes = [i32]
     L.vox_last_error.restype = C.c_char_p
@@ -90,7 +91,7 @@ def lib():
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
                  "vox_copy_level", "vox_copy_level_acc", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
-                 "vox_stats_get", "vox_stats_reset", "vox_sync"):
+                 "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -286,6 +287,10 @@ class Vox:
 
     def sync(self):
         self._check(lib().vox_sync(self._h), "sync")
+
+    def trim(self):
+        """Release the library's cached device blocks of this stream."""
+        self._check(lib().vox_trim(self._h), "trim")
 
 
 def _dist_ready(group) -> bool:

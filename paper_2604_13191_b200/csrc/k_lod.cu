@@ -127,7 +127,8 @@ __global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* _
 // are a contiguous block of leaf rows, loaded with coalesced 8-byte words into shared memory;
 // each lane then reduces its own parent from shared memory, and the outputs are staged and
 // written back as contiguous words. Same arithmetic as k_lod_prep (exact integer sums).
-constexpr int PREP_WARPS = 4;
+constexpr int PREP_WARPS = 8;
+constexpr int PREP_PAR = 16;   // parents per warp (their children fit 128 staged rows)
 
 template <int K>
 __global__ void __launch_bounds__(PREP_WARPS * 32)
@@ -142,12 +143,12 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int x = threadIdx.x; x <= MAXN; x += blockDim.x) s_hist[x] = 0;
     __syncthreads();
-    long long* rows = s_dyn + (size_t)wib * (256 * 7 + 32 * 7 + 32 * K * 7);
-    long long* sacc = rows + 256 * 7;
-    long long* slob = sacc + 32 * 7;
-    for (uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * 32; p0 < V;
-         p0 += (uint64_t)gridDim.x * PREP_WARPS * 32) {
-        const uint64_t pe = p0 + 32 < V ? p0 + 32 : V;
+    long long* rows = s_dyn + (size_t)wib * (8 * PREP_PAR * 7 + PREP_PAR * 7 + PREP_PAR * K * 7);
+    long long* sacc = rows + 8 * PREP_PAR * 7;
+    long long* slob = sacc + PREP_PAR * 7;
+    for (uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * PREP_PAR; p0 < V;
+         p0 += (uint64_t)gridDim.x * PREP_WARPS * PREP_PAR) {
+        const uint64_t pe = p0 + PREP_PAR < V ? p0 + PREP_PAR : V;
         const int np = (int)(pe - p0);
         const uint32_t cs = start[p0], ce = start[pe];
         const int nw = (int)(ce - cs) * 7;
@@ -208,17 +209,30 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
 
 // Exclusive offsets of the per-n buckets (ascending n) and the split between the quad
 // kernel (n <= 8) and the warp kernel (n > 8). counts = {n_small, n_total}.
+// Also accumulates the level's algorithmic SGGX-H work into work[3] (sigma evaluations:
+// n + (n - K); distance evaluations: n(n-1)/2 + sum over merges of (m - 2); hard parents).
 __global__ void k_bucket_init(const unsigned* __restrict__ hist, int K, int maxn, unsigned* __restrict__ cursor,
-                              unsigned* __restrict__ counts) {
+                              unsigned* __restrict__ counts, unsigned long long* __restrict__ work) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     unsigned off = 0, small = 0;
+    unsigned long long sg = 0, dd = 0, hp = 0;
     for (int n = K + 1; n <= maxn; n++) {
         cursor[n] = off;
         off += hist[n];
         if (n <= 8) small = off;
+        unsigned long long d = (unsigned long long)n * (n - 1) / 2;
+        for (int m = n; m > K; m--) d += (unsigned long long)(m - 2);
+        sg += (unsigned long long)hist[n] * (unsigned long long)(2 * n - K);
+        dd += (unsigned long long)hist[n] * d;
+        hp += hist[n];
     }
     counts[0] = small;
     counts[1] = off;
+    if (work) {
+        work[0] += sg;
+        work[1] += dd;
+        work[2] += hp;
+    }
 }
 
 constexpr int SCATTER_PER_THREAD = 8;
@@ -740,9 +754,9 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     CK(cudaMemsetAsync(hist, 0, 4 * (MAXN + 1), c->stream));
     timer_begin(c, c->t_prep);
     if (leaf) {
-        uint64_t pb = ((V + 31) / 32 + PREP_WARPS - 1) / PREP_WARPS;
+        uint64_t pb = ((V + PREP_PAR - 1) / PREP_PAR + PREP_WARPS - 1) / PREP_WARPS;
         pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 16);
-        const size_t psm = (size_t)PREP_WARPS * (256 * 7 + 32 * 7 + 32 * K * 7) * sizeof(long long);
+        const size_t psm = (size_t)PREP_WARPS * (8 * PREP_PAR * 7 + PREP_PAR * 7 + PREP_PAR * K * 7) * sizeof(long long);
         CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
         k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.key, C.acc, start, V, P.key, P.acc,
                                                                             P.mass, P.m6, P.ncl, P.clacc, P.cl,
@@ -752,7 +766,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
                                                          P.acc, P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
     }
     timer_end(c, c->t_prep);
-    k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts);
+    k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts, c->d_lodwork);
     const uint64_t sb = (V + 256ull * SCATTER_PER_THREAD - 1) / (256ull * SCATTER_PER_THREAD);
     k_bucket_scatter<<<(unsigned)(sb ? sb : 1), 256, 0, c->stream>>>(nlob, V, K, MAXN, cursor, list);
     c->st.launches += 3;
@@ -778,21 +792,6 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         c->st.launches++;
     }
     CK(cudaGetLastError());
-    if (c->profile) {
-        // algorithmic SGGX-H work of this level from the per-n histogram: sigma evaluations
-        // (n initial + one per merge) and distance evaluations (n(n-1)/2 initial + m-2 per
-        // merge at size m), each a pinned sequence of fp32 operations
-        std::vector<unsigned> h(MAXN + 1);
-        CK(cudaMemcpyAsync(h.data(), hist, 4 * (MAXN + 1), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        for (int n = K + 1; n <= MAXN; n++) {
-            uint64_t sg = (uint64_t)n + (uint64_t)(n - K), dd = (uint64_t)n * (n - 1) / 2;
-            for (int m = n; m > K; m--) dd += (uint64_t)(m - 2);
-            c->st.lod_sigma_evals += (uint64_t)h[n] * sg;
-            c->st.lod_dist_evals += (uint64_t)h[n] * dd;
-            c->st.lod_hard_parents += h[n];
-        }
-    }
     dfree(c, list);
     dfree(c, hist);
     dfree(c, nlob);
@@ -820,7 +819,7 @@ vox_status build_level(vox_ctx* c, int l) {
     c->st.launches += 2;
     uint32_t V = 0;
     CK(cudaMemcpyAsync(&V, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     CK(dalloc(c, (void**)&start, ((uint64_t)V + 1) * 4));
     k_pstarts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
     c->st.launches++;
@@ -918,7 +917,7 @@ vox_status unpack_level(vox_ctx* c, int level, const void* buf, uint64_t n) {
     c->st.launches++;
     unsigned fl = 0;
     CK(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     if (fl) {
         c->err = "import: records not strictly ascending or bad lobe count";
         free_level(c, L);

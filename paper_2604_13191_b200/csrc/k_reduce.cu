@@ -81,7 +81,7 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     c->st.launches += 2;   // scan init + scan
     uint32_t V32 = 0;
     CK(cudaMemcpyAsync(&V32, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     CK(dalloc(c, (void**)&start, ((uint64_t)V32 + 1) * 4));
     k_starts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
     c->st.launches++;
@@ -181,7 +181,7 @@ __global__ void k_bin_caps(const unsigned long long* __restrict__ Wb, uint64_t n
     }
 }
 
-constexpr int BIN_THREADS = 256;
+constexpr int BIN_THREADS = 128;
 
 // Compact list of the non-empty bins (order irrelevant: every bin writes its own slots).
 __global__ void k_bin_active(const unsigned* __restrict__ cnt, uint64_t nb, unsigned* __restrict__ list,
@@ -234,9 +234,10 @@ k_bin_count(const uint64_t* __restrict__ keys, const unsigned long long* __restr
     }
 }
 
-constexpr int BIN_NMAX = 16384;   // pairs of a bin handled by the in-shared-memory counting sort
-constexpr int BIN_VMAX = 12288;   // distinct keys of such a bin
-constexpr int BIN_CHUNK = 1024;   // voxels per pass of the fallback path (larger bins)
+constexpr int BIN_NMAX = 6144;    // pairs of a bin handled by the in-shared-memory counting sort
+constexpr int BIN_VMAX = 4096;    // distinct keys of such a bin (a 16^3 bin has at most 4096)
+constexpr int BIN_CHUNK = 384;    // voxels per pass of the fallback path (bins with more pairs)
+constexpr int BIN_WORDS = 1024;   // bitmap words reserved (32^3 bins)
 
 // exclusive prefix of popcounts of the bitmap words (block scan over <= 1024 words)
 __device__ __forceinline__ void bitmap_prefix(const unsigned* bm, unsigned* wpre, int words, unsigned* s_wsum) {
@@ -306,8 +307,8 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
     unsigned* bm = reinterpret_cast<unsigned*>(s_raw);                      // [words]
-    unsigned* wpre = bm + 1024;                                             // [words]
-    unsigned* cur = wpre + 1024;                                            // [BIN_VMAX + 1]
+    unsigned* wpre = bm + words;                                            // [words]
+    unsigned* cur = wpre + words;                                           // [BIN_VMAX + 1]
     unsigned short* sidx = reinterpret_cast<unsigned short*>(cur + BIN_VMAX + 1);   // [BIN_NMAX]
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(cur);   // fallback: [BIN_CHUNK][7]
     unsigned short* lkey = reinterpret_cast<unsigned short*>(acc + BIN_CHUNK * 7);   // fallback: [BIN_CHUNK]
@@ -419,7 +420,7 @@ vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::v
     c->st.launches++;
     WT.resize(nT);
     CK(cudaMemcpyAsync(WT.data(), dWT, nT * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     dfree(c, dWT);
     return VOX_OK;
 }
@@ -441,7 +442,7 @@ vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigne
     c->st.launches += 3;
     unsigned long long cap = 0;
     CK(cudaMemcpyAsync(&cap, off + nb, 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     dfree(c, tmp);
     dfree(c, caps);
     *off_out = off;
@@ -468,7 +469,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     CK(cudaMemsetAsync(npairs, 0, 16, c->stream));
     CK(cudaMemsetAsync(vcount, 0, (nb + 1) * 4, c->stream));
     k_bin_active<<<grid_for(nb), 256, 0, c->stream>>>(bins.cnt, nb, alist, nact);
-    const unsigned grid = (unsigned)std::min<uint64_t>(nb, 148ull * 8);
+    const unsigned grid = (unsigned)std::min<uint64_t>(nb, 148ull * 16);
     k_bin_count<<<grid, BIN_THREADS, words * 4, c->stream>>>(keys, bins.off, bins.cnt, alist, nact, lbits, vcount,
                                                              npairs);
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, vcount, voff, (int64_t)(nb + 1), c->stream));
@@ -479,7 +480,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     unsigned long long P = 0;
     CK(cudaMemcpyAsync(&V, voff + nb, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&P, npairs, 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(ssync(c));
     timer_end(c, c->t_sort);
     c->st.pairs = P;
     timer_begin(c, c->t_reduce);
@@ -490,7 +491,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     CK(dalloc(c, (void**)&nacc, (uint64_t)V * 56));
     CK(dalloc(c, (void**)&nmass, (uint64_t)V * 4));
     CK(dalloc(c, (void**)&nm6, (uint64_t)V * 24));
-    const size_t smem = 2 * 1024 * 4 + (BIN_VMAX + 1) * 4 + BIN_NMAX * 2 + 16;
+    const size_t smem = 2 * (size_t)words * 4 + (BIN_VMAX + 1) * 4 + BIN_NMAX * 2 + 16;
     static_assert(BIN_CHUNK * 7 * 8 + BIN_CHUNK * 2 <= (BIN_VMAX + 1) * 4 + BIN_NMAX * 2, "fallback must fit");
     CK(cudaFuncSetAttribute(k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_bin_reduce<<<grid, BIN_THREADS, smem, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact, voff,

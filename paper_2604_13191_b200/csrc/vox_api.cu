@@ -4,20 +4,101 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <map>
+#include <unordered_map>
+#include <mutex>
 #include <new>
 
 #include "vox_internal.cuh"
 
 namespace vox {
 
+double host_ms_since(const std::chrono::steady_clock::time_point& t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Device memory: a process-wide caching allocator (best fit within 2x, per stream). Blocks
+// freed by a call go back to the cache and are reused by later calls on the same stream, so
+// stream order makes reuse safe; cudaMallocAsync is only hit on a cache miss (its pool showed
+// multi-10-ms stalls when the same sizes were requested step after step). vox_trim releases.
+struct CachedBlock {
+    cudaStream_t stream;
+    size_t bytes;
+};
+static std::mutex g_mem_mu;
+static std::multimap<std::pair<cudaStream_t, size_t>, void*> g_free;   // (stream, bytes) -> ptr
+static std::unordered_map<void*, CachedBlock> g_live;
+
+static size_t round_bytes(size_t b) {
+    if (b <= 4096) return 4096;
+    if (b <= (1u << 20)) {   // powers of two up to 1 MiB
+        size_t r = 4096;
+        while (r < b) r <<= 1;
+        return r;
+    }
+    return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);   // 2 MiB granularity
+}
+
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
     *p = nullptr;
-    if (bytes == 0) bytes = 16;
-    return cudaMallocAsync(p, bytes, c->stream);
+    const size_t want = round_bytes(bytes ? bytes : 16);
+    const auto t0 = std::chrono::steady_clock::now();
+    {
+        std::lock_guard<std::mutex> lk(g_mem_mu);
+        auto it = g_free.lower_bound({c->stream, want});
+        if (it != g_free.end() && it->first.first == c->stream && it->first.second <= 2 * want) {
+            *p = it->second;
+            g_live[*p] = CachedBlock{c->stream, it->first.second};
+            g_free.erase(it);
+        }
+    }
+    cudaError_t e = cudaSuccess;
+    if (!*p) {
+        e = cudaMallocAsync(p, want, c->stream);
+        if (e == cudaErrorMemoryAllocation) {   // release cached blocks of this stream and retry
+            cudaGetLastError();
+            vox_trim_stream(c->stream);
+            e = cudaMallocAsync(p, want, c->stream);
+        }
+        if (e == cudaSuccess) {
+            std::lock_guard<std::mutex> lk(g_mem_mu);
+            g_live[*p] = CachedBlock{c->stream, want};
+        }
+    }
+    c->st.host_ms_alloc += host_ms_since(t0);
+    return e;
 }
 
 void dfree(vox_ctx* c, void* p) {
-    if (p) cudaFreeAsync(p, c->stream);
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    auto it = g_live.find(p);
+    if (it == g_live.end()) {   // not ours (should not happen)
+        cudaFreeAsync(p, c->stream);
+        return;
+    }
+    g_free.insert({{it->second.stream, it->second.bytes}, p});
+    g_live.erase(it);
+}
+
+void vox_trim_stream(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    for (auto it = g_free.begin(); it != g_free.end();) {
+        if (it->first.first == s) {
+            cudaFreeAsync(it->second, s);
+            it = g_free.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+cudaError_t ssync(vox_ctx* c) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    c->st.host_ms_sync += host_ms_since(t0);
+    return e;
 }
 
 void free_level(vox_ctx* c, Level& L) {
@@ -26,27 +107,50 @@ void free_level(vox_ctx* c, Level& L) {
     L = Level();
 }
 
+// Timing events are recycled process-wide: creating events costs tens of microseconds,
+// which would add up over the ~200 stage events of one voxelize + LoD build.
+static std::mutex g_ev_mu;
+static std::vector<cudaEvent_t> g_ev_pool;
+
+static cudaEvent_t event_get(vox_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_ev_mu);
+        if (!g_ev_pool.empty()) {
+            cudaEvent_t e = g_ev_pool.back();
+            g_ev_pool.pop_back();
+            return e;
+        }
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
 void timer_begin(vox_ctx* c, StageTimer& t) {
     if (!c->profile) return;
-    cudaEventCreate(&t.open);
+    t.open = event_get(c);
     cudaEventRecord(t.open, c->stream);
 }
 
 void timer_end(vox_ctx* c, StageTimer& t) {
     if (!c->profile || !t.open) return;
-    cudaEvent_t b;
-    cudaEventCreate(&b);
+    cudaEvent_t b = event_get(c);
     cudaEventRecord(b, c->stream);
     t.done.emplace_back(t.open, b);
     t.open = nullptr;
 }
 
-static double timer_flush(StageTimer& t) {
+static double timer_flush(vox_ctx* c, StageTimer& t) {
     for (auto& pr : t.done) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) t.ms += ms;
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
+        c->ev_pool.push_back(pr.first);
+        c->ev_pool.push_back(pr.second);
     }
     t.done.clear();
     return t.ms;
@@ -76,6 +180,8 @@ static vox_status ensure_dev(vox_ctx* c) {
     CKS(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     CKS(cudaMallocAsync((void**)&c->d_flags, 16, c->stream));
     CKS(cudaMallocAsync((void**)&c->d_counter, 16, c->stream));
+    CKS(cudaMallocAsync((void**)&c->d_lodwork, 32, c->stream));
+    CKS(cudaMemsetAsync(c->d_lodwork, 0, 32, c->stream));
     upload_theta(c);
     CKS(cudaGetLastError());
     return VOX_OK;
@@ -168,7 +274,8 @@ vox_status vox_plan_shards(const uint64_t* w, uint64_t ncells, int world, uint64
 typedef cudaError_t (*emit_fn)(vox_ctx*, const float*, const float*, uint64_t, Shard, Bins, uint64_t*, uint64_t*,
                                float4*);
 
-static int bin_log2(const vox_ctx* c) { return std::min(5, c->g.logN - c->T); }
+// bins of 16^3 voxels (32^3 at 8192^3 to bound the bin arrays), never coarser than a top cell
+static int bin_log2(const vox_ctx* c) { return std::min(c->g.logN >= 13 ? 5 : 4, c->g.logN - c->T); }
 static uint64_t nbins_of(const vox_ctx* c) { return 1ull << (3 * (c->g.logN - bin_log2(c))); }
 
 static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* Wb,
@@ -177,7 +284,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     const int Lb = bin_log2(c);
     unsigned fl = 0;
     CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CKS(cudaStreamSynchronize(c->stream));
+    CKS(ssync(c));
     timer_end(c, c->t_bound);
     if (fl) {
         dfree(c, Wb);
@@ -250,7 +357,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     timer_end(c, c->t_emit);
     s = reduce_bins(c, keys, vals, bins, nb, ptab);
     CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CKS(cudaStreamSynchronize(c->stream));
+    CKS(ssync(c));
     dfree(c, keys);
     dfree(c, vals);
     dfree(c, ptab);
@@ -429,7 +536,7 @@ vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass
         dfree(c, dn);
         dfree(c, dc);
     }
-    CKS(cudaStreamSynchronize(c->stream));
+    CKS(ssync(c));
     return VOX_OK;
 }
 
@@ -439,7 +546,7 @@ vox_status vox_copy_level_acc(vox_ctx* c, uint32_t level, int64_t* acc) {
     const Level& L = c->lv[level];
     if (L.n == 0) return VOX_OK;
     CKS(cudaMemcpyAsync(acc, L.acc, L.n * 56, cudaMemcpyDefault, c->stream));
-    CKS(cudaStreamSynchronize(c->stream));
+    CKS(ssync(c));
     return VOX_OK;
 }
 
@@ -484,19 +591,26 @@ vox_status vox_theta_table(float* theta, float* coef) {
 
 vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     if (!c || !out) return VOX_ERR_INVALID_ARG;
-    CKS(cudaStreamSynchronize(c->stream));
-    c->st.ms_bound = timer_flush(c->t_bound);
-    c->st.ms_emit = timer_flush(c->t_emit);
-    c->st.ms_sort = timer_flush(c->t_sort);
-    c->st.ms_reduce = timer_flush(c->t_reduce);
-    c->st.ms_merge = timer_flush(c->t_merge);
-    c->st.ms_lod_scan = timer_flush(c->t_lodscan);
-    c->st.ms_lod = timer_flush(c->t_lod);
-    c->st.ms_total_vox = timer_flush(c->t_vox);
-    c->st.ms_total_lod = timer_flush(c->t_lodall);
-    c->st.ms_lod_prep = timer_flush(c->t_prep);
-    c->st.ms_sggxh_quad = timer_flush(c->t_quad);
-    c->st.ms_sggxh_warp = timer_flush(c->t_warp);
+    CKS(ssync(c));
+    c->st.ms_bound = timer_flush(c, c->t_bound);
+    c->st.ms_emit = timer_flush(c, c->t_emit);
+    c->st.ms_sort = timer_flush(c, c->t_sort);
+    c->st.ms_reduce = timer_flush(c, c->t_reduce);
+    c->st.ms_merge = timer_flush(c, c->t_merge);
+    c->st.ms_lod_scan = timer_flush(c, c->t_lodscan);
+    c->st.ms_lod = timer_flush(c, c->t_lod);
+    c->st.ms_total_vox = timer_flush(c, c->t_vox);
+    c->st.ms_total_lod = timer_flush(c, c->t_lodall);
+    c->st.ms_lod_prep = timer_flush(c, c->t_prep);
+    c->st.ms_sggxh_quad = timer_flush(c, c->t_quad);
+    c->st.ms_sggxh_warp = timer_flush(c, c->t_warp);
+    if (c->d_lodwork) {
+        unsigned long long w[3] = {0, 0, 0};
+        CKS(cudaMemcpy(w, c->d_lodwork, 24, cudaMemcpyDeviceToHost));
+        c->st.lod_sigma_evals = w[0];
+        c->st.lod_dist_evals = w[1];
+        c->st.lod_hard_parents = w[2];
+    }
     *out = c->st;
     return VOX_OK;
 }
@@ -509,28 +623,44 @@ vox_status vox_stats_reset(vox_ctx* c) {
                           &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp})
         t->ms = 0.0;
     c->st.launches = 0;
+    c->st.host_ms_alloc = c->st.host_ms_sync = 0;
     c->st.lod_sigma_evals = c->st.lod_dist_evals = c->st.lod_hard_parents = 0;
+    if (c->d_lodwork) CKS(cudaMemsetAsync(c->d_lodwork, 0, 32, c->stream));
+    return VOX_OK;
+}
+
+vox_status vox_trim(vox_ctx* c) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    CKS(ssync(c));
+    vox_trim_stream(c->stream);
+    CKS(ssync(c));
     return VOX_OK;
 }
 
 vox_status vox_sync(vox_ctx* c) {
     if (!c) return VOX_ERR_INVALID_ARG;
-    CKS(cudaStreamSynchronize(c->stream));
+    CKS(ssync(c));
     return VOX_OK;
 }
 
 void vox_destroy(vox_ctx* c) {
     if (!c) return;
-    cudaStreamSynchronize(c->stream);
+    ssync(c);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
                           &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp}) {
-        timer_flush(*t);
+        timer_flush(c, *t);
         if (t->open) cudaEventDestroy(t->open);
     }
+    {
+        std::lock_guard<std::mutex> lk(g_ev_mu);
+        for (cudaEvent_t e : c->ev_pool) g_ev_pool.push_back(e);
+    }
+    c->ev_pool.clear();
+    if (c->d_lodwork) cudaFreeAsync(c->d_lodwork, c->stream);
     if (c->d_flags) cudaFreeAsync(c->d_flags, c->stream);
     if (c->d_counter) cudaFreeAsync(c->d_counter, c->stream);
-    cudaStreamSynchronize(c->stream);
+    ssync(c);
     delete c;
 }
 

@@ -153,6 +153,8 @@ struct vox_ctx {
     uint64_t cell_lo = 0, cell_hi = 0;
     vox::Level lv[VOX_MAX_LEVELS];
     unsigned int* d_flags = nullptr;        // device error flags
+    unsigned long long* d_lodwork = nullptr; // [3]: SGGX-H sigma evals, distance evals, hard parents (profile)
+    std::vector<cudaEvent_t> ev_pool;       // recycled timing events (profile)
     unsigned long long* d_counter = nullptr; // pair cursor
     vox_stats st{};
     std::string err;
@@ -164,7 +166,9 @@ namespace vox {
 
 // allocation helpers (stream-ordered)
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes);
+cudaError_t ssync(vox_ctx* c);   // cudaStreamSynchronize with host-time accounting
 void dfree(vox_ctx* c, void* p);
+void vox_trim_stream(cudaStream_t s);   // release the allocation cache of a stream
 void free_level(vox_ctx* c, Level& L);
 void timer_begin(vox_ctx* c, StageTimer& t);
 void timer_end(vox_ctx* c, StageTimer& t);
