@@ -193,6 +193,55 @@ __device__ __forceinline__ bool far_from_capsule(const Fib& f, const float* d, f
 // ---------------------------------------------------------------- emit
 
 constexpr int EMIT_WARPS = 8;
+// Evaluates the first nq (<= 32) queued candidates, one per lane: the pinned predicate and
+// l_r (§4), the exact S_acc contribution (segmented scan over lanes: queue order keeps the
+// owner segments non-decreasing) and the binned append of in-grid, in-shard keys.
+__device__ __forceinline__ void eval_queue(const int4* q, int nq, int lane, float (*sf)[32],
+                                           unsigned long long* sacc, uint64_t batch, const GridXf& g,
+                                           const Shard& sh, const Bins& bins, uint64_t* __restrict__ keys,
+                                           uint64_t* __restrict__ vals, unsigned* __restrict__ flags) {
+    bool emit = false;
+    uint64_t mkey = 0, val = 0;
+    long long qv = 0;
+    int o = 32;
+    if (lane < nq) {
+        const int4 e = q[lane];
+        o = e.x;
+        const int64_t i = e.y, j = e.z, k = e.w;
+        Fib fo;
+        for (int ax = 0; ax < 3; ax++) {
+            fo.a[ax] = sf[ax][o];
+            fo.w[ax] = sf[3 + ax][o];
+            fo.iota[ax] = sf[6 + ax][o];
+        }
+        fo.r2 = sf[9][o];
+        fo.moving = __float_as_uint(sf[10][o]);
+        fo.len = sf[11][o];
+        float ell;
+        if (fiber_key(fo, i, j, k, ell)) {
+            qv = q32(ell);
+            if (i >= 0 && j >= 0 && k >= 0 && i < g.N && j < g.N && k < g.N) {
+                mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
+                const uint64_t cell = mkey >> sh.shift;
+                if (cell >= sh.cell_lo && cell < sh.cell_hi) {
+                    emit = true;
+                    val = (batch * 32 + o) | ((uint64_t)__float_as_uint(ell) << 32);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, qv, dlt);
+        const int oy = __shfl_up_sync(0xffffffffu, o, dlt);
+        if (lane >= dlt && oy == o) qv += y;
+    }
+    const int onext = __shfl_down_sync(0xffffffffu, o, 1);
+    if (o < 32 && (lane == 31 || onext != o)) sacc[o] += (unsigned long long)qv;
+    if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
+    __syncwarp();
+}
+
 // One warp per batch of 32 consecutive segments. The batch's candidate voxels (the
 // unclamped AABB ranges, §3) are flattened and dealt round-robin to the 32 lanes, so every
 // lane evaluates one (segment, voxel) candidate per step whatever the segment sizes.
@@ -207,6 +256,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
     __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
     __shared__ uint32_t s_start[EMIT_WARPS][32];
     __shared__ unsigned long long s_acc[EMIT_WARPS][32];
+    __shared__ int4 s_q[EMIT_WARPS][64];   // survivor FIFO: (segment lane, i, j, k)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nbatch = (S + 31) / 32;
     const float PI_F = 3.14159274101257324f;   // 0x40490FDB
@@ -262,14 +312,16 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
         s_acc[wib][lane] = 0ull;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         __syncwarp();
+        // Pass over the flattened candidates: cheap index math + conservative early reject;
+        // survivors go to a per-warp FIFO in candidate order and are evaluated 32 at a time, so
+        // the expensive pinned predicate runs on full warps.
+        int qn = 0;
         for (uint32_t c0 = 0; c0 < total; c0 += 32) {
             const uint32_t c = c0 + lane;
-            bool emit = false;
-            uint64_t mkey = 0, val = 0;
-            long long qv = 0;
-            int o = 32;   // owner segment of this lane's candidate (32 = none)
+            bool surv = false;
+            int o = 0;
+            int4 ent = make_int4(0, 0, 0, 0);
             if (c < total) {
-                o = 0;
 #pragma unroll
                 for (int step = 16; step; step >>= 1)
                     if (s_start[wib][o + step] <= c) o += step;
@@ -284,37 +336,23 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                 for (int ax = 0; ax < 3; ax++) {
                     fo.a[ax] = s_f[wib][ax][o];
                     fo.w[ax] = s_f[wib][3 + ax][o];
-                    fo.iota[ax] = s_f[wib][6 + ax][o];
                     dv[ax] = s_f[wib][12 + ax][o];
                 }
-                fo.r2 = s_f[wib][9][o];
-                fo.moving = __float_as_uint(s_f[wib][10][o]);
-                fo.len = s_f[wib][11][o];
-                float ell;
-                if (!far_from_capsule(fo, dv, s_f[wib][15][o], i, j, k) && fiber_key(fo, i, j, k, ell)) {
-                    qv = q32(ell);
-                    if (i >= 0 && j >= 0 && k >= 0 && i < g.N && j < g.N && k < g.N) {
-                        mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
-                        const uint64_t cell = mkey >> sh.shift;
-                        if (cell >= sh.cell_lo && cell < sh.cell_hi) {
-                            emit = true;
-                            val = (batch * 32 + o) | ((uint64_t)__float_as_uint(ell) << 32);
-                        }
-                    }
-                }
+                surv = !far_from_capsule(fo, dv, s_f[wib][15][o], i, j, k);
+                ent = make_int4(o, (int)i, (int)j, (int)k);
             }
-            // exact S_acc: segmented inclusive scan over lanes of the same segment (owners are
-            // non-decreasing along the lanes), then one plain add by each segment's last lane
-#pragma unroll
-            for (int dlt = 1; dlt < 32; dlt <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, qv, dlt);
-                const int oy = __shfl_up_sync(0xffffffffu, o, dlt);
-                if (lane >= dlt && oy == o) qv += y;
+            const unsigned bal = __ballot_sync(0xffffffffu, surv);
+            if (surv) s_q[wib][qn + __popc(bal & ((1u << lane) - 1u))] = ent;
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn >= 32) {
+                eval_queue(s_q[wib], 32, lane, s_f[wib], s_acc[wib], batch, g, sh, bins, keys, vals, flags);
+                if (lane < qn - 32) s_q[wib][lane] = s_q[wib][32 + lane];
+                qn -= 32;
+                __syncwarp();
             }
-            const int onext = __shfl_down_sync(0xffffffffu, o, 1);
-            if (o < 32 && (lane == 31 || onext != o)) s_acc[wib][o] += (unsigned long long)qv;
-            if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
         }
+        if (qn) eval_queue(s_q[wib], qn, lane, s_f[wib], s_acc[wib], batch, g, sh, bins, keys, vals, flags);
         __syncwarp();
         if (p < S) {
             // §5 per-segment normalisation f_p = m_p / S_p and unit tangent
