@@ -1,0 +1,93 @@
+"""Parity at BASELINE.json's full sizes, in bench.py's launch configuration, on sampled
+outputs: the GPU builds the whole config; the oracle recomputes whole Morton cells (every
+primitive touching a cell, LoD inside it) and every level <= the cell level is compared
+bit-for-bit inside those cells (windowed parity)."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _cells(keys0, level, count, rng):
+    cells, cnt = np.unique(keys0 >> np.uint64(3 * level), return_counts=True)
+    order = np.argsort(-cnt, kind="stable")
+    pick = [cells[order[0]], cells[order[len(order) // 2]]]          # densest and a median cell
+    pick += list(rng.choice(cells, size=max(0, count - 2), replace=False))
+    return [int(c) for c in pick]
+
+
+def _window_oracle(c, level, cell):
+    N, bbox = c["grid_res"], c["bbox"]
+    E = float(np.max(bbox[3:] - bbox[:3]))
+    i, j, k = oracle.unmorton(cell)
+    lo_box = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
+    hi_box = lo_box + ((1 << level) + 4) * E / N
+    o = oracle.Oracle(N, bbox)
+    o.set_window(level, cell)
+    if c["kind"] == "fiber":
+        s, r = c["segments"], c["radii"]
+        lo = np.minimum(s[:, 0], s[:, 1]) - r[:, None]
+        hi = np.maximum(s[:, 0], s[:, 1]) + r[:, None]
+        sel = np.all((hi >= lo_box) & (lo <= hi_box), axis=1)
+        o.add_fibers(np.ascontiguousarray(s[sel]), np.ascontiguousarray(r[sel]))
+    else:
+        t = c["tris"]
+        sel = np.all((t.max(1) >= lo_box) & (t.min(1) <= hi_box), axis=1)
+        d = None if c["dirs"] is None else np.ascontiguousarray(c["dirs"][sel])
+        o.add_triangles(np.ascontiguousarray(t[sel]), d)
+    o.build(level)
+    return o
+
+
+def _check(v, c, level, cells):
+    levels = [v.level(l) for l in range(level + 1)]      # device copies; cells selected on the GPU
+    for cell in cells:
+        o = _window_oracle(c, level, cell)
+        for l in range(level + 1):
+            g = levels[l]
+            sel = (g["key"] >> (3 * (level - l))) == cell
+            r = o.level(l)
+            assert np.array_equal(g["key"][sel].cpu().numpy().astype(np.uint64), r["key"]), (cell, l, "keys")
+            assert np.array_equal(g["acc"][sel].cpu().numpy(), r["acc"]), (cell, l, "acc")
+            assert np.array_equal(g["mass"][sel].cpu().numpy(), r["mass"]), (cell, l, "mass")
+            if l > 0:
+                assert np.array_equal(g["ncl"][sel].cpu().numpy(), r["ncl"]), (cell, l, "ncl")
+                assert np.array_equal(g["cl"][sel].cpu().numpy(), r["cl"]), (cell, l, "cl")
+        o.close()
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2604_13191_b200 import build
+    build.build()
+    import paper_2604_13191_b200 as P
+    return P
+
+
+def test_config4_fullsize_windowed(P):
+    c = gen.config(4)                                   # 10.28M segments at 4096^3, bench workload
+    v = P.Vox(c["grid_res"], c["bbox"])
+    v.voxelize_fibers(torch.from_numpy(c["segments"]).cuda(), torch.from_numpy(c["radii"]).cuda())
+    v.build_lod(c["levels"])
+    L0 = v.level(0)
+    k0 = L0["key"].cpu().numpy().astype(np.uint64)
+    assert len(k0) > 10_000_000
+    # mass conservation at full size (exact integers), every level
+    tot = L0["acc"].sum(0)
+    del L0
+    for l in range(1, c["levels"] + 1):
+        assert torch.equal(v.level(l)["acc"].sum(0), tot)
+    _check(v, c, 6, _cells(k0, 6, 4, np.random.default_rng(0)))
+
+
+def test_config3_fullsize_windowed(P):
+    c = gen.config(3)                                   # 100,352 triangles at 2048^3, tangent mode
+    v = P.Vox(c["grid_res"], c["bbox"])
+    v.voxelize_triangles(torch.from_numpy(c["tris"]).cuda(), torch.from_numpy(c["dirs"]).cuda())
+    v.build_lod(c["levels"])
+    k0 = v.level(0)["key"].cpu().numpy().astype(np.uint64)
+    _check(v, c, 7, _cells(k0, 7, 3, np.random.default_rng(1)))
