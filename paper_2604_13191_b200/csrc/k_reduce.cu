@@ -410,6 +410,103 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
     }
 }
 
+// Warp-per-bin variant for the common small bins (no block barriers): each warp owns a bin
+// of <= WB_NMAX pairs and <= WB_VMAX distinct keys with a private bitmap / rank table in
+// shared memory. Bins above the limits are listed for k_bin_reduce (block per bin).
+constexpr int WB_WARPS = 4;
+constexpr int WB_NMAX = 1536;
+constexpr int WB_VMAX = 1024;
+
+__global__ void __launch_bounds__(WB_WARPS * 32)
+k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals,
+                  const float4* __restrict__ ptab, const unsigned long long* __restrict__ off,
+                  const unsigned* __restrict__ cnt, const unsigned* __restrict__ alist,
+                  const unsigned* __restrict__ nact, const unsigned* __restrict__ voff, int lbits,
+                  unsigned* __restrict__ big, unsigned* __restrict__ nbig, uint64_t* __restrict__ okey,
+                  long long* __restrict__ oacc, float* __restrict__ omass, float* __restrict__ om6) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const size_t per_warp = (size_t)2 * words * 4 + (WB_VMAX + 1) * 4 + WB_NMAX * 2;
+    unsigned* bm = reinterpret_cast<unsigned*>(s_raw + wib * per_warp);
+    unsigned* wpre = bm + words;
+    unsigned* cur = wpre + words;
+    unsigned short* sidx = reinterpret_cast<unsigned short*>(cur + WB_VMAX + 1);
+    const uint64_t lmask = (1ull << lbits) - 1ull;
+    const unsigned na = *nact;
+    for (unsigned ai = blockIdx.x * WB_WARPS + wib; ai < na; ai += gridDim.x * WB_WARPS) {
+        const unsigned b = alist[ai];
+        const unsigned n = cnt[b];
+        const unsigned vb = voff[b], V = voff[b + 1] - vb;
+        if (n > WB_NMAX || V > WB_VMAX) {
+            if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+            continue;
+        }
+        const uint64_t o = off[b];
+        for (int w = lane; w < words; w += 32) bm[w] = 0u;
+        for (unsigned r = lane; r <= V; r += 32) cur[r] = 0u;
+        __syncwarp();
+        for (unsigned i = lane; i < n; i += 32) {
+            const unsigned lk = (unsigned)(keys[o + i] & lmask);
+            atomicOr(&bm[lk >> 5], 1u << (lk & 31));
+        }
+        __syncwarp();
+        {   // exclusive popcount prefix over the words: contiguous chunk per lane + warp scan
+            const int per = (words + 31) / 32, w0 = lane * per;
+            unsigned loc = 0;
+            for (int q = 0; q < per; q++)
+                if (w0 + q < words) loc += __popc(bm[w0 + q]);
+            unsigned inc = loc;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            unsigned run = inc - loc;
+            for (int q = 0; q < per; q++)
+                if (w0 + q < words) {
+                    wpre[w0 + q] = run;
+                    run += __popc(bm[w0 + q]);
+                }
+        }
+        __syncwarp();
+        for (unsigned i = lane; i < n; i += 32)
+            atomicAdd(&cur[key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask)) + 1], 1u);
+        __syncwarp();
+        {   // inclusive scan of cur[0..V] -> cur[r] = first slot of rank r
+            const unsigned per = (V + 1 + 31) / 32, r0 = lane * per;
+            unsigned loc = 0;
+            for (unsigned q = 0; q < per; q++)
+                if (r0 + q <= V) loc += cur[r0 + q];
+            unsigned inc = loc;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            unsigned run = inc - loc;
+            for (unsigned q = 0; q < per; q++)
+                if (r0 + q <= V) {
+                    run += cur[r0 + q];
+                    cur[r0 + q] = run;
+                }
+        }
+        __syncwarp();
+        for (unsigned i = lane; i < n; i += 32) {
+            const unsigned r = key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask));
+            sidx[atomicAdd(&cur[r], 1u)] = (unsigned short)i;
+        }
+        __syncwarp();
+        for (unsigned r = lane; r < V; r += 32) {
+            const unsigned p0 = r == 0 ? 0u : cur[r - 1], p1 = cur[r];
+            long long a[7] = {0, 0, 0, 0, 0, 0, 0};
+            for (unsigned p = p0; p < p1; p++) add_pair(vals[o + sidx[p]], ptab, a);
+            emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc, omass, om6);
+        }
+        __syncwarp();
+    }
+}
+
 // Top-cell candidate counts (sum of the bins of each top cell) for the shard plan.
 vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT) {
     const uint64_t nT = 1ull << (3 * c->T);
@@ -491,12 +588,22 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     CK(dalloc(c, (void**)&nacc, (uint64_t)V * 56));
     CK(dalloc(c, (void**)&nmass, (uint64_t)V * 4));
     CK(dalloc(c, (void**)&nm6, (uint64_t)V * 24));
+    // small bins: warp per bin; the others (listed by it) then get a block each
+    unsigned* big = nullptr;
+    CK(dalloc(c, (void**)&big, nb * 4 + 4));
+    unsigned* nbig = big + nb;
+    CK(cudaMemsetAsync(nbig, 0, 4, c->stream));
+    const size_t wsm = (size_t)WB_WARPS * ((size_t)2 * words * 4 + (WB_VMAX + 1) * 4 + WB_NMAX * 2);
+    CK(cudaFuncSetAttribute(k_bin_reduce_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + WB_WARPS - 1) / WB_WARPS, 148ull * 32);
+    k_bin_reduce_warp<<<wgrid, WB_WARPS * 32, wsm, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact,
+                                                                voff, lbits, big, nbig, nkey, nacc, nmass, nm6);
     const size_t smem = 2 * (size_t)words * 4 + (BIN_VMAX + 1) * 4 + BIN_NMAX * 2 + 16;
     static_assert(BIN_CHUNK * 7 * 8 + BIN_CHUNK * 2 <= (BIN_VMAX + 1) * 4 + BIN_NMAX * 2, "fallback must fit");
     CK(cudaFuncSetAttribute(k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bin_reduce<<<grid, BIN_THREADS, smem, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact, voff,
+    k_bin_reduce<<<grid, BIN_THREADS, smem, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, big, nbig, voff,
                                                          lbits, nkey, nacc, nmass, nm6);
-    c->st.launches++;
+    c->st.launches += 2;
     CK(cudaGetLastError());
     timer_end(c, c->t_reduce);
     dfree(c, tmp);
@@ -504,6 +611,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     dfree(c, voff);
     dfree(c, npairs);
     dfree(c, alist);
+    dfree(c, big);
     c->st.voxels = V;
     return merge_into_leaf(c, nkey, nacc, nmass, nm6, V);
 }
