@@ -81,11 +81,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def _workload(cfg: int, n_segments: int | None):
+def _workload(cfg: int, n_segments: int | None, grid_res: int | None = None):
     import gen
     kw = {}
     if n_segments:
         kw["n_segments"] = n_segments
+    if grid_res and cfg == 5:
+        kw["grid_res"] = grid_res
     c = gen.config(cfg, **kw)
     return c
 
@@ -166,7 +168,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--segments", type=int, default=None, help="override the segment count (quick runs)")
+    ap.add_argument("--segments", type=int, default=None, help="override the segment count (config 4/5)")
+    ap.add_argument("--grid", type=int, default=None, help="grid resolution of a config-5 sweep point")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -191,7 +194,7 @@ def main():
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c = _workload(args.config, args.segments)
+    c = _workload(args.config, args.segments, args.grid)
     N, levels, bbox = c["grid_res"], c["levels"], c["bbox"]
     fib = c["kind"] == "fiber"
     if fib:
@@ -299,7 +302,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "segments/s" if fib else "triangles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config],
+            "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config]
+                       + (f" [point: {n_prims} segments at {N}^3]" if args.config == 5 else ""),
                        "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
                        "l2": "inputs (28 B x prims) larger than L2; no flush"},
             "lod_ms": stage["ms_total_lod"], "vox_ms": stage["ms_total_vox"],

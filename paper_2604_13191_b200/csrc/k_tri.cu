@@ -2,6 +2,8 @@
 // half-open clipped area emit (k_tri_emit). docs/PREDICATES.md §1, §3, §6, §7 (north star:
 // triangle-box SAT; P:225-228 area-weighted triangle sampling whose continuous limit is the
 // clipped area; P:179 face normals, P:183/P:549 tangent mode).
+#include <cub/cub.cuh>
+
 #include "vox_internal.cuh"
 
 namespace vox {
@@ -195,80 +197,105 @@ __device__ float tri_clip_area(const float* g, int64_t i, int64_t j, int64_t k) 
 
 // ---------------------------------------------------------------- emit
 
-constexpr int TRI_WARPS = 4;
+// Per-triangle setup (grid-space vertices, clamped candidate box, prim table entry) and the
+// candidate count; an exclusive scan of the counts then lets the emit kernel deal fixed-size
+// chunks of the global candidate space to warps, so one huge triangle or a handful of
+// triangles still spread over the whole GPU.
+struct TriSetup {
+    float g[9];
+    int e0[3];
+    unsigned ex, ey;
+    unsigned pad;
+};
 
-// One warp per batch of 32 triangles; the batch's clamped candidate voxels are flattened
-// and dealt round-robin to the lanes (same scheme as k_fiber_emit). Keys (SAT) emit
-// (key, prim | area) pairs; the prim table holds (d_hat, f = 1).
-__global__ void __launch_bounds__(TRI_WARPS * 32)
-k_tri_emit(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx, Shard sh,
-           Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab,
-           unsigned* __restrict__ flags) {
-    __shared__ float s_g[TRI_WARPS][9][32];
-    __shared__ int64_t s_e0[TRI_WARPS][3][32];
-    __shared__ uint32_t s_ex[TRI_WARPS][2][32];
-    __shared__ unsigned long long s_start[TRI_WARPS][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint64_t nbatch = (T + 31) / 32;
-    for (uint64_t batch = blockIdx.x * (uint64_t)TRI_WARPS + wib; batch < nbatch;
-         batch += (uint64_t)gridDim.x * TRI_WARPS) {
-        const uint64_t t = batch * 32 + lane;
+__global__ void k_tri_setup(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx,
+                            TriSetup* __restrict__ ts, unsigned long long* __restrict__ tcnt,
+                            float4* __restrict__ ptab) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
+        float v[9];
+        for (int q = 0; q < 9; q++) v[q] = tri[9 * t + q];
+        TriGeom G;
+        tri_geom(gx, v, G);
+        float dh[3];
+        tri_dir(G.g, dirs ? dirs + 3 * t : nullptr, dh);
+        ptab[t] = make_float4(dh[0], dh[1], dh[2], 1.0f);
+        TriSetup s;
+        for (int q = 0; q < 9; q++) s.g[q] = G.g[q];
         unsigned long long cnt = 0;
-        if (t < T) {
-            float v[9];
-            for (int q = 0; q < 9; q++) v[q] = tri[9 * t + q];
-            TriGeom G;
-            tri_geom(gx, v, G);
-            float dh[3];
-            tri_dir(G.g, dirs ? dirs + 3 * t : nullptr, dh);
-            ptab[t] = make_float4(dh[0], dh[1], dh[2], 1.0f);
-            if (!G.culled) {
-                cnt = (unsigned long long)(G.e1[0] - G.e0[0] + 1) * (unsigned long long)(G.e1[1] - G.e0[1] + 1) *
-                      (unsigned long long)(G.e1[2] - G.e0[2] + 1);
-                for (int ax = 0; ax < 3; ax++) s_e0[wib][ax][lane] = G.e0[ax];
-                s_ex[wib][0][lane] = (uint32_t)(G.e1[0] - G.e0[0] + 1);
-                s_ex[wib][1][lane] = (uint32_t)(G.e1[1] - G.e0[1] + 1);
-            }
-            for (int q = 0; q < 9; q++) s_g[wib][q][lane] = G.g[q];
+        if (!G.culled) {
+            for (int ax = 0; ax < 3; ax++) s.e0[ax] = (int)G.e0[ax];
+            s.ex = (unsigned)(G.e1[0] - G.e0[0] + 1);
+            s.ey = (unsigned)(G.e1[1] - G.e0[1] + 1);
+            cnt = (unsigned long long)s.ex * s.ey * (unsigned long long)(G.e1[2] - G.e0[2] + 1);
+        } else {
+            s.e0[0] = s.e0[1] = s.e0[2] = 0;
+            s.ex = s.ey = 1;
         }
-        unsigned long long incl = cnt;
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+        s.pad = 0;
+        ts[t] = s;
+        tcnt[t] = cnt;
+    }
+}
+
+constexpr int TRI_WARPS = 4;
+constexpr int TRI_CHUNK = 256;   // candidates per warp work item
+
+__device__ __forceinline__ uint64_t tri_upper(const unsigned long long* __restrict__ toff, uint64_t lo, uint64_t hi,
+                                              unsigned long long c) {
+    // last t in [lo, hi) with toff[t] <= c
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (toff[mid] <= c) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Warps take TRI_CHUNK consecutive candidates of the global (triangle-major) candidate space;
+// each lane locates its triangle by a binary search bounded by the chunk's first/last triangle.
+// Keys (SAT, §6) emit (key, prim | clipped area (§7)) pairs into their bins.
+__global__ void __launch_bounds__(TRI_WARPS * 32)
+k_tri_emit(const TriSetup* __restrict__ ts, const unsigned long long* __restrict__ toff, uint64_t T, GridXf gx,
+           Shard sh, Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals,
+           unsigned* __restrict__ flags) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned long long total = toff[T];
+    const unsigned long long nchunk = (total + TRI_CHUNK - 1) / TRI_CHUNK;
+    for (unsigned long long ch = blockIdx.x * (unsigned long long)TRI_WARPS + wib; ch < nchunk;
+         ch += (unsigned long long)gridDim.x * TRI_WARPS) {
+        const unsigned long long cb = ch * TRI_CHUNK;
+        const unsigned long long ce = cb + TRI_CHUNK < total ? cb + TRI_CHUNK : total;
+        uint64_t tlo = 0, thi = 0;
+        if (lane == 0) {
+            tlo = tri_upper(toff, 0, T, cb);
+            thi = tri_upper(toff, tlo, T, ce - 1) + 1;
         }
-        s_start[wib][lane] = incl - cnt;
-        const unsigned long long total = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-        for (unsigned long long c0 = 0; c0 < total; c0 += 32) {
+        tlo = __shfl_sync(0xffffffffu, tlo, 0);
+        thi = __shfl_sync(0xffffffffu, thi, 0);
+        for (unsigned long long c0 = cb; c0 < ce; c0 += 32) {
             const unsigned long long c = c0 + lane;
             bool emit = false;
             uint64_t mkey = 0, val = 0;
-            if (c < total) {
-                int o = 0;
-#pragma unroll
-                for (int step = 16; step; step >>= 1)
-                    if (s_start[wib][o + step] <= c) o += step;
-                const unsigned long long local = c - s_start[wib][o];
-                const unsigned long long ex = s_ex[wib][0][o], ey = s_ex[wib][1][o];
-                const unsigned long long q = local / ex;
-                const int64_t i = s_e0[wib][0][o] + (int64_t)(local - q * ex);
-                const int64_t j = s_e0[wib][1][o] + (int64_t)(q % ey);
-                const int64_t k = s_e0[wib][2][o] + (int64_t)(q / ey);
-                float g[9];
-                for (int m = 0; m < 9; m++) g[m] = s_g[wib][m][o];
-                if (tri_box_sat(g, i, j, k)) {
+            if (c < ce) {
+                const uint64_t t = tri_upper(toff, tlo, thi, c);
+                const TriSetup s = ts[t];
+                const unsigned long long local = c - toff[t];
+                const unsigned long long q = local / s.ex;
+                const int64_t i = s.e0[0] + (int64_t)(local - q * s.ex);
+                const int64_t j = s.e0[1] + (int64_t)(q % s.ey);
+                const int64_t k = s.e0[2] + (int64_t)(q / s.ey);
+                if (tri_box_sat(s.g, i, j, k)) {
                     mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
                     const uint64_t cell = mkey >> sh.shift;
                     if (cell >= sh.cell_lo && cell < sh.cell_hi) {
-                        const float A = tri_clip_area(g, i, j, k);
+                        const float A = tri_clip_area(s.g, i, j, k);
                         emit = true;
-                        val = (batch * 32 + o) | ((uint64_t)__float_as_uint(A) << 32);
+                        val = t | ((uint64_t)__float_as_uint(A) << 32);
                     }
                 }
             }
             if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
         }
-        __syncwarp();
     }
 }
 
@@ -284,13 +311,30 @@ cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, ui
 
 cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, Bins bins,
                             uint64_t* keys, uint64_t* vals, float4* ptab) {
-    const uint64_t nbatch = (T + 31) / 32;
-    uint64_t blocks = (nbatch + TRI_WARPS - 1) / TRI_WARPS;
-    if (blocks > (1ull << 30)) blocks = 1ull << 30;
-    k_tri_emit<<<(unsigned)blocks, TRI_WARPS * 32, 0, c->stream>>>(tri, dirs, T, c->g, sh, bins, keys, vals, ptab,
-                                                                   c->d_flags);
-    c->st.launches++;
-    return cudaGetLastError();
+    TriSetup* ts = nullptr;
+    unsigned long long *tcnt = nullptr, *toff = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    cudaError_t e;
+    if ((e = dalloc(c, (void**)&ts, T * sizeof(TriSetup))) != cudaSuccess) return e;
+    if ((e = dalloc(c, (void**)&tcnt, (T + 1) * 8)) != cudaSuccess) return e;
+    if ((e = dalloc(c, (void**)&toff, (T + 1) * 8)) != cudaSuccess) return e;
+    uint64_t blocks = (T + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    k_tri_setup<<<(unsigned)blocks, 256, 0, c->stream>>>(tri, dirs, T, c->g, ts, tcnt, ptab);
+    if ((e = cudaMemsetAsync(tcnt + T, 0, 8, c->stream)) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt, toff, (int64_t)(T + 1), c->stream)) != cudaSuccess)
+        return e;
+    if ((e = dalloc(c, &tmp, tb)) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tcnt, toff, (int64_t)(T + 1), c->stream)) != cudaSuccess) return e;
+    k_tri_emit<<<148u * 16, TRI_WARPS * 32, 0, c->stream>>>(ts, toff, T, c->g, sh, bins, keys, vals, c->d_flags);
+    c->st.launches += 4;
+    e = cudaGetLastError();
+    dfree(c, tmp);
+    dfree(c, toff);
+    dfree(c, tcnt);
+    dfree(c, ts);
+    return e;
 }
 
 }  // namespace vox
