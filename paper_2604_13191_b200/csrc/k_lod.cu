@@ -330,7 +330,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
              uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl) {
     __shared__ long long s_lobe[QUAD_WARPS][4][8][7];
-    __shared__ float s_S[QUAD_WARPS][4][8][6];
+    __shared__ __align__(16) float s_S[QUAD_WARPS][4][8][6];
     __shared__ float s_D[QUAD_WARPS][4][28];
     __shared__ uint16_t s_pair[28];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -344,7 +344,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     long long(*lobe)[7] = s_lobe[wib][g];
     float(*Sg)[6] = s_S[wib][g];
     float* D = s_D[wib][g];
-    __shared__ float s_cf[32][6];
+    __shared__ __align__(16) float s_cf[32][6];
     for (int x = threadIdx.x; x < 32 * 6; x += blockDim.x) s_cf[x / 6][x % 6] = c_coef[x / 6][x % 6];
     __syncthreads();
     const unsigned small = counts[0];
@@ -412,19 +412,28 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         __syncwarp();
         float sg[8][4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            float cq[6];
+        for (int c = 0; c < 8; c++)
 #pragma unroll
-            for (int e = 0; e < 6; e++) cq[e] = s_cf[l + 8 * q][e];
+            for (int q = 0; q < 4; q++) sg[c][q] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float2* cfr = reinterpret_cast<const float2*>(s_cf[l + 8 * q]);
+            const float2 c01 = cfr[0], c23 = cfr[1], c45 = cfr[2];
 #pragma unroll
             for (int c = 0; c < 8; c++) {
+                if (c >= nmax) break;
                 float qq = 0.0f;
-                if (c < nmax && valid && c < n) {
-                    qq = cq[0] * Sg[c][0];
-#pragma unroll
-                    for (int e = 1; e < 6; e++) qq = qq + cq[e] * Sg[c][e];
+                if (valid && c < n) {
+                    const float2* sr = reinterpret_cast<const float2*>(Sg[c]);
+                    const float2 s01 = sr[0], s23 = sr[1], s45 = sr[2];
+                    qq = c01.x * s01.x;
+                    qq = qq + c01.y * s01.y;
+                    qq = qq + c23.x * s23.x;
+                    qq = qq + c23.y * s23.y;
+                    qq = qq + c45.x * s45.x;
+                    qq = qq + c45.y * s45.y;
                 }
-                sg[c][q] = (c < nmax) ? sqrtf(pmax(qq, 0.0f)) : 0.0f;
+                sg[c][q] = sqrtf(pmax(qq, 0.0f));
             }
         }
 #pragma unroll
@@ -530,6 +539,27 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
     return v[0];
 }
 
+// d(i, j) with four lanes per pair over rows stored by slice residue class mod 4 (lane c4 =
+// class): lane c4 sums slices c4, c4+4, ..., c4+28 in the pinned tree's first three levels
+// (h = 16, 8, 4 pair slices of the same class), then levels h = 2 and 1 are xor-shuffles in the
+// 4-lane group -- exactly the pinned association (PREDICATES §9).
+__device__ __forceinline__ float dist4(const float* ri, const float* rj, int c4) {
+    const float4* a = reinterpret_cast<const float4*>(ri + 8 * c4);
+    const float4* b = reinterpret_cast<const float4*>(rj + 8 * c4);
+    const float4 a0 = a[0], a1 = a[1], b0 = b[0], b1 = b[1];
+    // m-th element of the class = slice c4 + 4m; level 16 pairs (m, m+4), 8 (m, m+2), 4 (m, m+1)
+    float s0 = fabsf(a0.x - b0.x) + fabsf(a1.x - b1.x);
+    float s1 = fabsf(a0.y - b0.y) + fabsf(a1.y - b1.y);
+    float s2 = fabsf(a0.z - b0.z) + fabsf(a1.z - b1.z);
+    float s3 = fabsf(a0.w - b0.w) + fabsf(a1.w - b1.w);
+    s0 = s0 + s2;
+    s1 = s1 + s3;
+    float s = s0 + s1;
+    s = s + __shfl_xor_sync(0xffffffffu, s, 2);
+    s = s + __shfl_xor_sync(0xffffffffu, s, 1);
+    return s;
+}
+
 constexpr int LOD_WARPS = 4;
 constexpr int SIG_STRIDE = 36;   // sigma rows (16-byte aligned): 8 distinct rows per LDS.128 wavefront
 
@@ -572,6 +602,9 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     float cf[6];
 #pragma unroll
     for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
+    // sigma rows are stored by slice residue class mod 4: position (k mod 4) * 8 + k / 4
+    const int spos = (lane & 3) * 8 + (lane >> 2);
+    const int g8 = lane >> 2, c4 = lane & 3;   // pair slot and residue class of this lane
     const unsigned lo = counts[0], hi = counts[1];
     for (unsigned w = lo + blockIdx.x * LOD_WARPS + wib; w < hi; w += gridDim.x * LOD_WARPS) {
         const uint64_t p = list[w];
@@ -592,29 +625,15 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             float q = cf[0] * Sm[c][0];
 #pragma unroll
             for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[c][e];
-            sig[c][lane] = sqrtf(pmax(q, 0.0f));
+            sig[c][spos] = sqrtf(pmax(q, 0.0f));
         }
         __syncwarp();
-        // ---- initial distance matrix: one pair per lane, the pinned tree evaluated in
-        // registers from two 32-slice sigma rows read as float4 (PREDICATES §9)
-        for (int t = lane; t < np; t += 32) {
-            const int pr = ptab[t];
-            const float4* ri = reinterpret_cast<const float4*>(sig[pr >> 8]);
-            const float4* rj = reinterpret_cast<const float4*>(sig[pr & 0xff]);
-            float sv[32];
-#pragma unroll
-            for (int k4 = 0; k4 < 8; k4++) {
-                const float4 a = ri[k4], b = rj[k4];
-                sv[4 * k4 + 0] = fabsf(a.x - b.x);
-                sv[4 * k4 + 1] = fabsf(a.y - b.y);
-                sv[4 * k4 + 2] = fabsf(a.z - b.z);
-                sv[4 * k4 + 3] = fabsf(a.w - b.w);
-            }
-#pragma unroll
-            for (int h = 16; h >= 1; h >>= 1)
-#pragma unroll
-                for (int q = 0; q < h; q++) sv[q] = sv[q] + sv[q + h];
-            D[t] = ((unsigned long long)__float_as_uint(sv[0]) << 32) | (unsigned)pr;
+        // ---- initial distance matrix: four lanes per pair (8 pairs per pass), see dist4
+        for (int t0 = 0; t0 < np; t0 += 8) {
+            const int t = t0 + g8;
+            const int pr = ptab[t < np ? t : 0];
+            const float d = dist4(sig[pr >> 8], sig[pr & 0xff], c4);
+            if (c4 == 0 && t < np) D[t] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)pr;
         }
         __syncwarp();
         // ---- SGGX-H merges: argmin of d over i < j, first in row-major order (D18)
@@ -637,30 +656,18 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 float q = cf[0] * Sm[bi][0];
 #pragma unroll
                 for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[bi][e];
-                sig[bi][lane] = sqrtf(pmax(q, 0.0f));
+                sig[bi][spos] = sqrtf(pmax(q, 0.0f));
             }
             __syncwarp();
-            // new row d(bi, x): one pair per lane, the pinned tree in registers from two
-            // float4-read sigma rows (the merged row is a broadcast read)
-            for (int x = lane; x < n; x += 32) {
-                if (x == bi || !((alive >> x) & 1ull)) continue;
-                const float4* ri = reinterpret_cast<const float4*>(sig[bi]);
-                const float4* rx = reinterpret_cast<const float4*>(sig[x]);
-                float sv[32];
-#pragma unroll
-                for (int k4 = 0; k4 < 8; k4++) {
-                    const float4 u = ri[k4], w = rx[k4];
-                    sv[4 * k4 + 0] = fabsf(u.x - w.x);
-                    sv[4 * k4 + 1] = fabsf(u.y - w.y);
-                    sv[4 * k4 + 2] = fabsf(u.z - w.z);
-                    sv[4 * k4 + 3] = fabsf(u.w - w.w);
+            // new row d(bi, x): four lanes per pair, 8 pairs per pass
+            for (int x0 = 0; x0 < n; x0 += 8) {
+                const int x = x0 + g8;
+                const int xr = x < n ? x : bi;
+                const float d = dist4(sig[bi], sig[xr], c4);
+                if (c4 == 0 && x < n && x != bi && ((alive >> x) & 1ull)) {
+                    const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                    D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)((a2 << 8) | b2);
                 }
-#pragma unroll
-                for (int h = 16; h >= 1; h >>= 1)
-#pragma unroll
-                    for (int q = 0; q < h; q++) sv[q] = sv[q] + sv[q + h];
-                const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
-                D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(sv[0]) << 32) | (unsigned)((a2 << 8) | b2);
             }
             // retire every pair of bj
             for (int x = lane; x < n; x += 32)
