@@ -539,25 +539,24 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// d(i, j) with four lanes per pair over rows stored by slice residue class mod 4 (lane c4 =
-// class): lane c4 sums slices c4, c4+4, ..., c4+28 in the pinned tree's first three levels
-// (h = 16, 8, 4 pair slices of the same class), then levels h = 2 and 1 are xor-shuffles in the
-// 4-lane group -- exactly the pinned association (PREDICATES §9).
-__device__ __forceinline__ float dist4(const float* ri, const float* rj, int c4) {
-    const float4* a = reinterpret_cast<const float4*>(ri + 8 * c4);
-    const float4* b = reinterpret_cast<const float4*>(rj + 8 * c4);
-    const float4 a0 = a[0], a1 = a[1], b0 = b[0], b1 = b[1];
-    // m-th element of the class = slice c4 + 4m; level 16 pairs (m, m+4), 8 (m, m+2), 4 (m, m+1)
-    float s0 = fabsf(a0.x - b0.x) + fabsf(a1.x - b1.x);
-    float s1 = fabsf(a0.y - b0.y) + fabsf(a1.y - b1.y);
-    float s2 = fabsf(a0.z - b0.z) + fabsf(a1.z - b1.z);
-    float s3 = fabsf(a0.w - b0.w) + fabsf(a1.w - b1.w);
-    s0 = s0 + s2;
-    s1 = s1 + s3;
-    float s = s0 + s1;
-    s = s + __shfl_xor_sync(0xffffffffu, s, 2);
-    s = s + __shfl_xor_sync(0xffffffffu, s, 1);
-    return s;
+// d(i, j) of two 32-slice sigma rows (float4 reads), the pinned tree in registers (PREDICATES §9)
+__device__ __forceinline__ float dist_row(const float* ri, const float* rj) {
+    const float4* a = reinterpret_cast<const float4*>(ri);
+    const float4* b = reinterpret_cast<const float4*>(rj);
+    float sv[32];
+#pragma unroll
+    for (int k4 = 0; k4 < 8; k4++) {
+        const float4 u = a[k4], w = b[k4];
+        sv[4 * k4 + 0] = fabsf(u.x - w.x);
+        sv[4 * k4 + 1] = fabsf(u.y - w.y);
+        sv[4 * k4 + 2] = fabsf(u.z - w.z);
+        sv[4 * k4 + 3] = fabsf(u.w - w.w);
+    }
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1)
+#pragma unroll
+        for (int q = 0; q < h; q++) sv[q] = sv[q] + sv[q + h];
+    return sv[0];
 }
 
 constexpr int LOD_WARPS = 4;
@@ -602,9 +601,6 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     float cf[6];
 #pragma unroll
     for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
-    // sigma rows are stored by slice residue class mod 4: position (k mod 4) * 8 + k / 4
-    const int spos = (lane & 3) * 8 + (lane >> 2);
-    const int g8 = lane >> 2, c4 = lane & 3;   // pair slot and residue class of this lane
     const unsigned lo = counts[0], hi = counts[1];
     for (unsigned w = lo + blockIdx.x * LOD_WARPS + wib; w < hi; w += gridDim.x * LOD_WARPS) {
         const uint64_t p = list[w];
@@ -625,15 +621,15 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             float q = cf[0] * Sm[c][0];
 #pragma unroll
             for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[c][e];
-            sig[c][spos] = sqrtf(pmax(q, 0.0f));
+            sig[c][lane] = sqrtf(pmax(q, 0.0f));
         }
         __syncwarp();
-        // ---- initial distance matrix: four lanes per pair (8 pairs per pass), see dist4
-        for (int t0 = 0; t0 < np; t0 += 8) {
-            const int t = t0 + g8;
-            const int pr = ptab[t < np ? t : 0];
-            const float d = dist4(sig[pr >> 8], sig[pr & 0xff], c4);
-            if (c4 == 0 && t < np) D[t] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)pr;
+        // ---- initial distance matrix: one pair per lane, the pinned tree evaluated in
+        // registers from two 32-slice sigma rows read as float4 (PREDICATES §9)
+        for (int t = lane; t < np; t += 32) {
+            const int pr = ptab[t];
+            const float d = dist_row(sig[pr >> 8], sig[pr & 0xff]);
+            D[t] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)pr;
         }
         __syncwarp();
         // ---- SGGX-H merges: argmin of d over i < j, first in row-major order (D18)
@@ -656,18 +652,15 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 float q = cf[0] * Sm[bi][0];
 #pragma unroll
                 for (int e = 1; e < 6; e++) q = q + cf[e] * Sm[bi][e];
-                sig[bi][spos] = sqrtf(pmax(q, 0.0f));
+                sig[bi][lane] = sqrtf(pmax(q, 0.0f));
             }
             __syncwarp();
-            // new row d(bi, x): four lanes per pair, 8 pairs per pass
-            for (int x0 = 0; x0 < n; x0 += 8) {
-                const int x = x0 + g8;
-                const int xr = x < n ? x : bi;
-                const float d = dist4(sig[bi], sig[xr], c4);
-                if (c4 == 0 && x < n && x != bi && ((alive >> x) & 1ull)) {
-                    const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
-                    D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)((a2 << 8) | b2);
-                }
+            // new row d(bi, x): one pair per lane (the merged row is a broadcast read)
+            for (int x = lane; x < n; x += 32) {
+                if (x == bi || !((alive >> x) & 1ull)) continue;
+                const float d = dist_row(sig[bi], sig[x]);
+                const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)((a2 << 8) | b2);
             }
             // retire every pair of bj
             for (int x = lane; x < n; x += 32)
