@@ -123,12 +123,41 @@ __global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* _
         if (s_hist[x]) atomicAdd(&hist[x], s_hist[x]);
 }
 
-// Level-1 prep (children are leaves): one warp per 32 consecutive parents. Their children
-// are a contiguous block of leaf rows, loaded with coalesced 8-byte words into shared memory;
-// each lane then reduces its own parent from shared memory, and the outputs are staged and
-// written back as contiguous words. Same arithmetic as k_lod_prep (exact integer sums).
-constexpr int PREP_WARPS = 8;
-constexpr int PREP_PAR = 16;   // parents per warp (their children fit 128 staged rows)
+// Level-1 prep (children are leaves): one warp per PREP_PAR consecutive parents. Their
+// children are one contiguous block of leaf rows; lane 0 fetches it into shared memory with a
+// single bulk async copy (cp.async.bulk, completion on an mbarrier), double-buffered so the
+// next block's copy is in flight while this one is reduced. Each lane then reduces its own
+// parent from shared memory, and the outputs are staged and written back as contiguous words.
+// Same arithmetic as k_lod_prep (exact integer sums). The copy is 16-byte aligned by starting
+// up to one 8-byte word early and rounding the size up; every device buffer carries >= 64 B of
+// allocation slack (dalloc), so the rounded tail stays inside the allocation.
+constexpr int PREP_WARPS = 4;
+constexpr int PREP_PAR = 16;                          // parents per warp-iteration
+constexpr int PREP_ROWW = 8 * PREP_PAR * 7 + 2;       // staged words per buffer (+ alignment)
+constexpr int PREP_WARP_WORDS = 2 * PREP_ROWW + PREP_PAR * 7 + 2;   // + acc staging; lobes added per K
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(b), "r"(phase)
+            : "memory");
+    }
+}
 
 template <int K>
 __global__ void __launch_bounds__(PREP_WARPS * 32)
@@ -138,26 +167,56 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
                 uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
                 uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
     constexpr int MAXN = 8 * K;
-    extern __shared__ __align__(16) long long s_dyn[];   // per warp: rows | acc | lobes
+    extern __shared__ __align__(16) long long s_dyn[];   // per warp: 2 x rows | acc | lobes
     __shared__ unsigned s_hist[MAXN + 1];
+    __shared__ uint64_t s_bar[PREP_WARPS][2];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int x = threadIdx.x; x <= MAXN; x += blockDim.x) s_hist[x] = 0;
+    if (lane == 0) {
+        mbar_init(&s_bar[wib][0], 1);
+        mbar_init(&s_bar[wib][1], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     __syncthreads();
-    long long* rows = s_dyn + (size_t)wib * (8 * PREP_PAR * 7 + PREP_PAR * 7 + PREP_PAR * K * 7);
-    long long* sacc = rows + 8 * PREP_PAR * 7;
-    long long* slob = sacc + PREP_PAR * 7;
-    for (uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * PREP_PAR; p0 < V;
-         p0 += (uint64_t)gridDim.x * PREP_WARPS * PREP_PAR) {
+    long long* wbase = s_dyn + (size_t)wib * (PREP_WARP_WORDS + PREP_PAR * K * 7);
+    long long* sacc = wbase + 2 * PREP_ROWW;
+    long long* slob = sacc + PREP_PAR * 7 + 2;
+    const uint64_t stride = (uint64_t)gridDim.x * PREP_WARPS * PREP_PAR;
+    uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * PREP_PAR;
+    // issue the bulk copy of block q0's children into buffer b; returns the word offset
+    auto issue = [&](uint64_t q0, int b) {
+        const uint64_t qe = q0 + PREP_PAR < V ? q0 + PREP_PAR : V;
+        const uint64_t w0 = 7 * (uint64_t)start[q0], w1 = 7 * (uint64_t)start[qe];
+        const uint64_t a0 = w0 & ~1ull;                      // 16-byte aligned start word
+        const unsigned bytes = (unsigned)(((w1 - a0) * 8 + 15) & ~15ull);
+        if (bytes) bulk_g2s(wbase + (size_t)b * PREP_ROWW, cacc + a0, bytes, &s_bar[wib][b]);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                              (unsigned)__cvta_generic_to_shared(&s_bar[wib][b])) : "memory");
+    };
+    if (lane == 0 && p0 < V) issue(p0, 0);
+    unsigned phase = 0;   // bit b: parity of buffer b's next completion
+    for (int it = 0; p0 < V; p0 += stride, it++) {
+        const int b = it & 1;
+        if (lane == 0 && p0 + stride < V) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(p0 + stride, b ^ 1);
+        }
         const uint64_t pe = p0 + PREP_PAR < V ? p0 + PREP_PAR : V;
         const int np = (int)(pe - p0);
-        const uint32_t cs = start[p0], ce = start[pe];
-        const int nw = (int)(ce - cs) * 7;
-        for (int w = lane; w < nw; w += 32) rows[w] = cacc[7 * (uint64_t)cs + w];
-        __syncwarp();
+        const uint32_t cs = start[p0];
+        int c0 = 0, c1 = 0;
+        uint64_t k0 = 0;
+        if (lane < np) {
+            c0 = (int)(start[p0 + lane] - cs);
+            c1 = (int)(start[p0 + lane + 1] - cs);
+            k0 = ckey[cs + c0];
+        }
+        mbar_wait(&s_bar[wib][b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        const long long* rows = wbase + (size_t)b * PREP_ROWW + ((7 * (uint64_t)cs) & 1);
         bool hard = false;
         if (lane < np) {
             const uint64_t p = p0 + lane;
-            const int c0 = (int)(start[p] - cs), c1 = (int)(start[p + 1] - cs);
             long long sum[7] = {0, 0, 0, 0, 0, 0, 0};
             int n = 0;
             for (int x = c0; x < c1; x++) {
@@ -165,7 +224,7 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
                 for (int e = 0; e < 7; e++) sum[e] += rows[7 * x + e];
                 n += rows[7 * x] > 0;
             }
-            pkey[p] = ckey[cs + c0] >> 3;
+            pkey[p] = k0 >> 3;
 #pragma unroll
             for (int e = 0; e < 7; e++) sacc[7 * lane + e] = sum[e];
             nlob[p] = (uint8_t)n;
@@ -755,8 +814,8 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     timer_begin(c, c->t_prep);
     if (leaf) {
         uint64_t pb = ((V + PREP_PAR - 1) / PREP_PAR + PREP_WARPS - 1) / PREP_WARPS;
-        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 16);
-        const size_t psm = (size_t)PREP_WARPS * (8 * PREP_PAR * 7 + PREP_PAR * 7 + PREP_PAR * K * 7) * sizeof(long long);
+        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 3);
+        const size_t psm = (size_t)PREP_WARPS * (PREP_WARP_WORDS + PREP_PAR * K * 7) * sizeof(long long);
         CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
         k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.key, C.acc, start, V, P.key, P.acc,
                                                                             P.mass, P.m6, P.ncl, P.clacc, P.cl,

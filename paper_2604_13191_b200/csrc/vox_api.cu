@@ -42,7 +42,7 @@ static size_t round_bytes(size_t b) {
 
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
     *p = nullptr;
-    const size_t want = round_bytes(bytes ? bytes : 16);
+    const size_t want = round_bytes((bytes ? bytes : 16) + 64);   // >= 64 B slack (bulk-copy tails)
     const auto t0 = std::chrono::steady_clock::now();
     {
         std::lock_guard<std::mutex> lk(g_mem_mu);
