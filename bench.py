@@ -236,7 +236,8 @@ def main():
             v = step(profile=True)
             st = v.stats()
             for k2 in ("ms_bound", "ms_emit", "ms_sort", "ms_reduce", "ms_merge", "ms_lod_scan", "ms_lod",
-                       "ms_total_vox", "ms_total_lod", "ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_warp"):
+                       "ms_total_vox", "ms_total_lod", "ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_half",
+                       "ms_sggxh_warp"):
                 stage[k2] = stage.get(k2, 0.0) + st[k2]
             launches += st["launches"]
             lodwork["sigma"] += st["lod_sigma_evals"]
@@ -277,7 +278,8 @@ def main():
         "radix_sort(pairs)": (stage["ms_sort"], "hbm", 32 * P),
         "segmented_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
         "k_lod_prep": (stage["ms_lod_prep"], "hbm", bytes_lod),
-        "k_sggxh_warp+quad": (stage["ms_sggxh_quad"] + stage["ms_sggxh_warp"], "alu", flops_sggxh),
+        "k_sggxh_quad+half+warp": (stage["ms_sggxh_quad"] + stage["ms_sggxh_half"] + stage["ms_sggxh_warp"], "alu",
+                                   flops_sggxh),
     }
     dom = max(kern, key=lambda k: kern[k][0])
     def roof_of(name):

@@ -76,7 +76,7 @@ typedef struct {
     uint64_t cell_lo, cell_hi; /* this rank's top-cell range [lo, hi) */
     /* accumulated device milliseconds per stage since the last vox_stats_reset (profile=1) */
     double ms_bound, ms_emit, ms_sort, ms_reduce, ms_merge, ms_lod_scan, ms_lod, ms_total_vox, ms_total_lod;
-    double ms_lod_prep, ms_sggxh_quad, ms_sggxh_warp;   /* parts of ms_lod */
+    double ms_lod_prep, ms_sggxh_quad, ms_sggxh_half, ms_sggxh_warp;   /* parts of ms_lod (n<=8, 9..16, >16) */
     uint64_t launches;     /* kernels launched by the library since the last reset */
     /* SGGX-H algorithmic work since the last reset (profile=1): lobe sigma evaluations
      * (32 slices each), pair distance evaluations (32 slices each), parents with n > k */

@@ -48,7 +48,8 @@ class _Stats(C.Structure):
                 ("ms_bound", C.c_double), ("ms_emit", C.c_double), ("ms_sort", C.c_double),
                 ("ms_reduce", C.c_double), ("ms_merge", C.c_double), ("ms_lod_scan", C.c_double),
                 ("ms_lod", C.c_double), ("ms_total_vox", C.c_double), ("ms_total_lod", C.c_double),
-                ("ms_lod_prep", C.c_double), ("ms_sggxh_quad", C.c_double), ("ms_sggxh_warp", C.c_double),
+                ("ms_lod_prep", C.c_double), ("ms_sggxh_quad", C.c_double),
+                ("ms_sggxh_half", C.c_double), ("ms_sggxh_warp", C.c_double),
                 ("launches", C.c_uint64), ("lod_sigma_evals", C.c_uint64), ("lod_dist_evals", C.c_uint64),
                 ("lod_hard_parents", C.c_uint64), ("host_ms_alloc", C.c_double), ("host_ms_sync", C.c_double)]
 

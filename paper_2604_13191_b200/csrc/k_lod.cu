@@ -273,20 +273,22 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
 __global__ void k_bucket_init(const unsigned* __restrict__ hist, int K, int maxn, unsigned* __restrict__ cursor,
                               unsigned* __restrict__ counts, unsigned long long* __restrict__ work) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    unsigned off = 0, small = 0;
+    unsigned off = 0, small = 0, mid = 0;
     unsigned long long sg = 0, dd = 0, hp = 0;
     for (int n = K + 1; n <= maxn; n++) {
         cursor[n] = off;
         off += hist[n];
         if (n <= 8) small = off;
+        if (n <= 16) mid = off;
         unsigned long long d = (unsigned long long)n * (n - 1) / 2;
         for (int m = n; m > K; m--) d += (unsigned long long)(m - 2);
         sg += (unsigned long long)hist[n] * (unsigned long long)(2 * n - K);
         dd += (unsigned long long)hist[n] * d;
         hp += hist[n];
     }
-    counts[0] = small;
-    counts[1] = off;
+    counts[0] = small;   // [0, small): n <= 8 (group kernel)
+    counts[1] = mid;     // [small, mid): 9 <= n <= 16 (half-warp kernel)
+    counts[2] = off;     // [mid, off): n > 16 (warp kernel)
     if (work) {
         work[0] += sg;
         work[1] += dd;
@@ -578,7 +580,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     }
 }
 
-// ---------------------------------------------------------------- SGGX-H, n > 8 (one warp per parent)
+// ---------------------------------------------------------------- SGGX-H, n > 16 (one warp per parent)
 // d(i,j) tree for 32 slices held one per lane, for 32 pairs at once ("transpose-reduce"):
 // lane p ends with the sum for pair p. At step h a lane keeps the half of its vector whose
 // pair index has bit h equal to its own and adds the partner's partial; the partial sums it
@@ -660,7 +662,7 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     float cf[6];
 #pragma unroll
     for (int e = 0; e < 6; e++) cf[e] = c_coef[lane][e];
-    const unsigned lo = counts[0], hi = counts[1];
+    const unsigned lo = counts[1], hi = counts[2];
     for (unsigned w = lo + blockIdx.x * LOD_WARPS + wib; w < hi; w += gridDim.x * LOD_WARPS) {
         const uint64_t p = list[w];
         // dendrogram leaves in child-slot order, w = 0 dropped (D17)
@@ -745,6 +747,169 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     }
 }
 
+// ---------------------------------------------------------------- SGGX-H, 9 <= n <= 16 (half warp per parent)
+// Two parents per warp, sixteen lanes each: the warp kernel's scheme at half width. Lane l
+// computes sigma for slices l and l+16; distances are one pair per lane from float4-read
+// sigma rows (dist_row, the pinned tree in registers); the argmin is a 16-lane xor reduce of
+// the packed (d, i, j) keys. Both halves run max(n) merge steps, a half with fewer lobes
+// idling through the surplus ones (bucket order makes the two n nearly always equal).
+constexpr int HALF_WARPS = 4;
+struct HalfPar {
+    long long lobe[16][7];
+    float S[16][6];
+    float sig[16][SIG_STRIDE];
+    unsigned long long D[120];
+};
+
+template <int K>
+__global__ void __launch_bounds__(HALF_WARPS * 32)
+k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
+             const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc,
+             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
+             float* __restrict__ pcl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t* ptab = reinterpret_cast<uint16_t*>(smem_raw);   // t -> (i << 8) | j, 120 entries
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane >> 4, l = lane & 15;
+    for (int t = threadIdx.x; t < 120; t += blockDim.x) {
+        int j = 1;
+        while ((j + 1) * j / 2 <= t) j++;
+        ptab[t] = (uint16_t)(((t - j * (j - 1) / 2) << 8) | j);
+    }
+    __syncthreads();
+    HalfPar& H = reinterpret_cast<HalfPar*>(smem_raw + 256)[2 * wib + g];
+    float cfa[6], cfb[6];
+#pragma unroll
+    for (int e = 0; e < 6; e++) {
+        cfa[e] = c_coef[l][e];
+        cfb[e] = c_coef[l + 16][e];
+    }
+    const unsigned lo = counts[0], hi = counts[1];
+    for (unsigned u = blockIdx.x * HALF_WARPS + wib; lo + 2 * u < hi; u += gridDim.x * HALF_WARPS) {
+        const unsigned idx = lo + 2 * u + g;
+        const bool valid = idx < hi;
+        const uint64_t p = valid ? list[idx] : 0;
+        uint32_t c0 = 0, c1 = 0;
+        if (valid) {
+            c0 = start[p];
+            c1 = start[p + 1];
+        }
+        // dendrogram leaves in child-slot order, w = 0 dropped (D17): rounds of 16 slots
+        const int slots = (int)(c1 - c0) * K;
+        int n = 0;
+        for (int b = 0; b < 8 * K; b += 16) {
+            const int sl = b + l;
+            bool has = false;
+            const long long* src = nullptr;
+            if (sl < slots) {
+                const uint64_t x = c0 + sl / K;
+                const int q = sl % K;
+                src = cclacc + (x * K + q) * 7;
+                has = q < cncl[x] && src[0] != 0;
+            }
+            const unsigned bal = (__ballot_sync(0xffffffffu, has) >> (16 * g)) & 0xffffu;
+            if (has) {
+                const int c = n + __popc(bal & ((1u << l) - 1u));
+#pragma unroll
+                for (int e = 0; e < 7; e++) H.lobe[c][e] = src[e];
+            }
+            n += __popc(bal);
+        }
+        __syncwarp();
+        const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+        unsigned alive = (1u << n) - 1u;
+        if (l < n) {
+            const float wf = deq32(H.lobe[l][0]);
+#pragma unroll
+            for (int e = 0; e < 6; e++) H.S[l][e] = deq32(H.lobe[l][1 + e]) / wf;
+        }
+        __syncwarp();
+        for (int c = 0; c < nmax; c++) {
+            if (c < n) {
+                float qa = cfa[0] * H.S[c][0], qb = cfb[0] * H.S[c][0];
+#pragma unroll
+                for (int e = 1; e < 6; e++) {
+                    qa = qa + cfa[e] * H.S[c][e];
+                    qb = qb + cfb[e] * H.S[c][e];
+                }
+                H.sig[c][l] = sqrtf(pmax(qa, 0.0f));
+                H.sig[c][l + 16] = sqrtf(pmax(qb, 0.0f));
+            }
+        }
+        __syncwarp();
+        const int np = n * (n - 1) / 2, npmax = nmax * (nmax - 1) / 2;
+        for (int t = l; t < npmax; t += 16) {
+            if (t < np) {
+                const int pr = ptab[t];
+                const float d = dist_row(H.sig[pr >> 8], H.sig[pr & 0xff]);
+                H.D[t] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)pr;
+            }
+        }
+        __syncwarp();
+        // ---- SGGX-H merges: argmin of d over i < j, first in row-major order (D18)
+        for (int m = nmax; m > K; m--) {
+            const bool act = m <= n;
+            unsigned long long best = ~0ull;
+            for (int t = l; t < npmax; t += 16) {
+                if (t < np) {
+                    const unsigned long long key = H.D[t];
+                    best = key < best ? key : best;
+                }
+            }
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+                best = y < best ? y : best;
+            }
+            const int bi = (int)((best >> 8) & 0xff), bj = (int)(best & 0xff);
+            if (act && l < 7) H.lobe[bi][l] += H.lobe[bj][l];   // exact moment merge (D15)
+            if (act) alive &= ~(1u << bj);
+            __syncwarp();
+            if (act && l < 6) H.S[bi][l] = deq32(H.lobe[bi][1 + l]) / deq32(H.lobe[bi][0]);
+            __syncwarp();
+            if (act) {
+                float qa = cfa[0] * H.S[bi][0], qb = cfb[0] * H.S[bi][0];
+#pragma unroll
+                for (int e = 1; e < 6; e++) {
+                    qa = qa + cfa[e] * H.S[bi][e];
+                    qb = qb + cfb[e] * H.S[bi][e];
+                }
+                H.sig[bi][l] = sqrtf(pmax(qa, 0.0f));
+                H.sig[bi][l + 16] = sqrtf(pmax(qb, 0.0f));
+            }
+            __syncwarp();
+            const int x = l;
+            if (act && x < n) {
+                if (x != bi && ((alive >> x) & 1u)) {   // new row d(bi, x)
+                    const float d = dist_row(H.sig[bi], H.sig[x]);
+                    const int a2 = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                    H.D[pair_t(a2, b2)] = ((unsigned long long)__float_as_uint(d) << 32) | (unsigned)((a2 << 8) | b2);
+                }
+                if (x != bj) {                            // retire every pair of bj
+                    const int a = x < bj ? x : bj, b2 = x < bj ? bj : x;
+                    H.D[pair_t(a, b2)] = ((unsigned long long)INF_BITS << 32) | (unsigned)((a << 8) | b2);
+                }
+            }
+            __syncwarp();
+        }
+        // output: surviving lobes in list order (K slots exactly, since n > K)
+        if (valid) {
+            int slot = 0;
+            for (int cc = 0; cc < n; cc++) {
+                if (!((alive >> cc) & 1u)) continue;
+                if (l < 7) {
+                    const long long a = H.lobe[cc][l];
+                    pclacc[(p * K + slot) * 7 + l] = a;
+                    pcl[(p * K + slot) * 7 + l] = deq32(a);
+                }
+                slot++;
+            }
+            if (l == 0) pncl[p] = (uint8_t)slot;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_pheads(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ flags) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         flags[i] = (i == 0 || (keys[i] >> 3) != (keys[i - 1] >> 3)) ? 1u : 0u;
@@ -806,7 +971,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     unsigned *hist = nullptr, *cursor = nullptr, *counts = nullptr;
     uint32_t* list = nullptr;
     CK(dalloc(c, (void**)&nlob, V));
-    CK(dalloc(c, (void**)&hist, 4 * (MAXN + 1) * 2 + 16));
+    CK(dalloc(c, (void**)&hist, 4 * (MAXN + 1) * 2 + 32));
     cursor = hist + (MAXN + 1);
     counts = cursor + (MAXN + 1);
     CK(dalloc(c, (void**)&list, V * 4));
@@ -840,6 +1005,17 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         c->st.launches++;
     }
     if (!leaf && MAXN > 8) {
+        const size_t smem = 256 + 2 * HALF_WARPS * sizeof(HalfPar);
+        CK(cudaFuncSetAttribute(k_sggxh_half<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        uint64_t hb = ((V + 1) / 2 + HALF_WARPS - 1) / HALF_WARPS;
+        hb = std::min<uint64_t>(std::max<uint64_t>(hb, 1), 148ull * 32);
+        timer_begin(c, c->t_half);
+        k_sggxh_half<K><<<(unsigned)hb, HALF_WARPS * 32, smem, c->stream>>>(list, counts, C.ncl, C.clacc, start,
+                                                                           P.ncl, P.clacc, P.cl);
+        timer_end(c, c->t_half);
+        c->st.launches++;
+    }
+    if (!leaf && MAXN > 16) {
         const size_t smem = LodSmem<K>::total;
         CK(cudaFuncSetAttribute(k_sggxh_warp<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         uint64_t wb = (V + LOD_WARPS - 1) / LOD_WARPS;

@@ -603,6 +603,7 @@ vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     c->st.ms_total_lod = timer_flush(c, c->t_lodall);
     c->st.ms_lod_prep = timer_flush(c, c->t_prep);
     c->st.ms_sggxh_quad = timer_flush(c, c->t_quad);
+    c->st.ms_sggxh_half = timer_flush(c, c->t_half);
     c->st.ms_sggxh_warp = timer_flush(c, c->t_warp);
     if (c->d_lodwork) {
         unsigned long long w[3] = {0, 0, 0};
@@ -620,7 +621,7 @@ vox_status vox_stats_reset(vox_ctx* c) {
     vox_stats tmp;
     vox_stats_get(c, &tmp);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp})
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp})
         t->ms = 0.0;
     c->st.launches = 0;
     c->st.host_ms_alloc = c->st.host_ms_sync = 0;
@@ -648,7 +649,7 @@ void vox_destroy(vox_ctx* c) {
     ssync(c);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_warp}) {
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp}) {
         timer_flush(c, *t);
         if (t->open) cudaEventDestroy(t->open);
     }

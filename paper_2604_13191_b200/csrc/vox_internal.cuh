@@ -159,7 +159,7 @@ struct vox_ctx {
     vox_stats st{};
     std::string err;
     // stage timers (profile = 1)
-    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_warp;
+    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp;
 };
 
 namespace vox {

@@ -17,7 +17,7 @@ for l in range(1, 13):
     idx = torch.searchsorted(cur["key"], pk)
     n = torch.zeros(len(cur["key"]), dtype=torch.long, device="cuda").index_add_(0, idx, lob)
     h = torch.bincount(n[n > 3], minlength=25).cpu().tolist()
-    print(l, "parents", len(n), "hard", int((n > 3).sum()), "quad", round(st["ms_sggxh_quad"], 2), "warp",
+    print(l, "parents", len(n), "hard", int((n > 3).sum()), "quad", round(st["ms_sggxh_quad"], 2), "half", round(st["ms_sggxh_half"], 2), "warp",
           round(st["ms_sggxh_warp"], 2), "prep", round(st["ms_lod_prep"], 2),
           {k: x for k, x in enumerate(h) if x}, flush=True)
     prev = cur
