@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 K_DEFAULT = 3
+HIST_N_DEFAULT = 5000   # P:389 "N=5000 samples for each S"
 
 
 def build(force: bool = False) -> str:
@@ -66,6 +67,14 @@ def lib():
         L.orc_sigma.argtypes = [i64p, f32p]
         L.orc_distance.restype = C.c_float
         L.orc_distance.argtypes = [i64p, i64p]
+        u16p = C.POINTER(C.c_uint16)
+        L.orc_set_distance.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.orc_sample_table.argtypes = [C.c_int, f32p]
+        L.orc_sw_tables.argtypes = [u8p, i64p]
+        L.orc_hist.argtypes = [i64p, C.c_int, u16p]
+        L.orc_hist_distance.restype = C.c_int64
+        L.orc_hist_distance.argtypes = [u16p, u16p]
+        L.orc_sggxh_hist.argtypes = [C.c_int, i64p, C.c_int, C.c_int, i64p]
         _lib = L
     return _lib
 
@@ -92,7 +101,8 @@ def _check(rc, what):
 class Oracle:
     """Plain CPU voxelizer + LoD builder (docs/PREDICATES.md §1-§9)."""
 
-    def __init__(self, grid_res: int, bbox, k: int = K_DEFAULT):
+    def __init__(self, grid_res: int, bbox, k: int = K_DEFAULT, distance: str = "sigma",
+                 hist_samples: int = HIST_N_DEFAULT):
         bb, p = _f32(np.asarray(bbox, dtype=np.float32).reshape(6))
         self._bb = bb
         self.k = int(k)
@@ -100,6 +110,9 @@ class Oracle:
         self._h = lib().orc_create(int(grid_res), p, int(k))
         if not self._h:
             raise OracleError("orc_create rejected (grid_res, bbox, k)")
+        if distance not in ("sigma", "hist"):
+            raise OracleError(f"unknown distance {distance!r}")
+        _check(lib().orc_set_distance(self._h, 1 if distance == "hist" else 0, int(hist_samples)), "set_distance")
 
     def close(self):
         if self._h:
@@ -212,6 +225,48 @@ def distance(a7, b7) -> float:
     a, ap = _i64(np.asarray(a7).reshape(7))
     b, bp = _i64(np.asarray(b7).reshape(7))
     return float(np.float32(lib().orc_distance(ap, bp)))
+
+
+# ----------------------------------------------------------------- §10 histogram distance
+
+def sample_table(n=HIST_N_DEFAULT):
+    """(n,3) fp32 whole-sphere spherical-Fibonacci sample points of §10."""
+    u = np.zeros((n, 3), np.float32)
+    lib().orc_sample_table(int(n), u.ctypes.data_as(C.POINTER(C.c_float)))
+    return u
+
+
+def sw_tables():
+    """(perm [32][125] uint8, gap [32][124] int64) slice tables of §10."""
+    perm = np.zeros((32, 125), np.uint8)
+    gap = np.zeros((32, 124), np.int64)
+    lib().orc_sw_tables(perm.ctypes.data_as(C.POINTER(C.c_uint8)), gap.ctypes.data_as(C.POINTER(C.c_int64)))
+    return perm, gap
+
+
+def hist(acc7, n=HIST_N_DEFAULT):
+    """125-bin histogram (uint16, bin = b0 + 5 b1 + 25 b2) of one cluster's n samples."""
+    a, ap = _i64(np.asarray(acc7).reshape(7))
+    h = np.zeros(125, np.uint16)
+    _check(lib().orc_hist(ap, int(n), h.ctypes.data_as(C.POINTER(C.c_uint16))), "hist")
+    return h
+
+
+def hist_distance(h1, h2) -> int:
+    a = np.ascontiguousarray(h1, dtype=np.uint16)
+    b = np.ascontiguousarray(h2, dtype=np.uint16)
+    return int(lib().orc_hist_distance(a.ctypes.data_as(C.POINTER(C.c_uint16)),
+                                       b.ctypes.data_as(C.POINTER(C.c_uint16))))
+
+
+def sggxh_hist(acc, k=K_DEFAULT, n=HIST_N_DEFAULT):
+    """SGGX-H with the histogram distance: (m,7) int64 -> kept clusters."""
+    a, ap = _i64(np.asarray(acc).reshape(-1, 7))
+    out = np.zeros((k, 7), np.int64)
+    m = lib().orc_sggxh_hist(a.shape[0], ap, int(k), int(n), out.ctypes.data_as(C.POINTER(C.c_int64)))
+    if m < 0:
+        raise OracleError(f"sggxh_hist status {m}")
+    return out[:m]
 
 
 Q = 2.0 ** 32

@@ -371,6 +371,17 @@ typedef struct {
     i128* cl;       /* [n][K][7] */
 } level_t;
 
+/* §10 tables (histogram distance mode), defined with the §10 code below */
+#define HIST_BINS 125
+#define HIST_NMIN 32
+#define HIST_NMAX 8160
+typedef struct hist_tables {
+    int N;
+    float (*u)[3];
+    uint8_t perm[32][HIST_BINS];
+    int64_t gap[32][HIST_BINS - 1];
+} hist_tables_t;
+
 typedef struct {
     grid_t g;
     int logN;
@@ -381,7 +392,12 @@ typedef struct {
     size_t nrec, cap;
     int built;                /* levels built (-1: nothing) */
     level_t lv[MAX_LEVELS];
+    int mode;                 /* 0: sigma distance (§9), 1: histogram distance (§10) */
+    int hist_n;               /* N samples per histogram (§10) */
+    struct hist_tables* ht;   /* §10 tables (mode 1) */
 } orc_ctx;
+
+static int hist_tables_init(hist_tables_t* T, int N);
 
 static int push_rec(orc_ctx* c, uint64_t key, const int64_t q[7]) {
     if (c->nrec == c->cap) {
@@ -414,13 +430,31 @@ orc_ctx* orc_create(uint32_t N, const float bbox[6], int K) {
     c->K = K;
     for (int a = 0; a < 3; a++) { c->wlo[a] = 0; c->whi[a] = (int64_t)N - 1; }
     c->built = -1;
+    c->mode = 0;
+    c->hist_n = 5000;
     return c;
+}
+
+/* §10: select the SGGX-H distance (0 sigma, 1 histogram with N samples per SGGX) */
+int orc_set_distance(orc_ctx* c, int mode, int N) {
+    if (mode < 0 || mode > 1 || N < HIST_NMIN || N > HIST_NMAX) return ORC_ERR_ARG;
+    if (mode == 1 && (!c->ht || c->ht->N != N)) {
+        if (c->ht) { free(c->ht->u); free(c->ht); c->ht = NULL; }
+        c->ht = (hist_tables_t*)calloc(1, sizeof(hist_tables_t));
+        if (!c->ht) return ORC_ERR_OOM;
+        int rc = hist_tables_init(c->ht, N);
+        if (rc != ORC_OK) { free(c->ht); c->ht = NULL; return rc; }
+    }
+    c->mode = mode;
+    c->hist_n = N;
+    return ORC_OK;
 }
 
 void orc_destroy(orc_ctx* c) {
     if (!c) return;
     free_levels(c);
     free(c->recs);
+    if (c->ht) { free(c->ht->u); free(c->ht); }
     free(c);
 }
 
@@ -697,6 +731,188 @@ float orc_distance(const int64_t a[7], const int64_t b[7]) {
     return sigma_dist(sa, sb);
 }
 
+/* ------------------------------------------------------------------ §10 histogram distance */
+/* distance_mode = hist: the paper's own distance, a Wasserstein
+ * distance between 5x5x5 histograms of N whole-sphere samples of each SGGX (P:383-389,
+ * P:341), taken as the sliced W1 over the 32 slices of §9 in exact
+ * integer arithmetic. Merges stay exact moment sums (D15); a merged cluster's histogram
+ * is drawn afresh from its S. */
+
+/* sample table: N spherical-Fibonacci points over the whole sphere, fp64 -> fp32 */
+static void sample_table(int N, float (*u)[3]) {
+    const double PI_D = 3.14159265358979323846;
+    const double ga = PI_D * (3.0 - sqrt(5.0));
+    for (int s = 0; s < N; s++) {
+        double z = 1.0 - (2.0 * s + 1.0) / N;
+        double rho = sqrt(1.0 - z * z);
+        double phi = s * ga;
+        u[s][0] = (float)(rho * cos(phi));
+        u[s][1] = (float)(rho * sin(phi));
+        u[s][2] = (float)z;
+    }
+}
+
+/* slice tables: fixed-point projections P[k][b] of the bin centres, bins sorted by
+ * (P, b) and the gaps between consecutive sorted projections */
+static void sw_tables(const float theta[32][3], uint8_t perm[32][HIST_BINS], int64_t gap[32][HIST_BINS - 1]) {
+    for (int k = 0; k < 32; k++) {
+        int64_t P[HIST_BINS];
+        int idx[HIST_BINS];
+        for (int b = 0; b < HIST_BINS; b++) {
+            int b0 = b % 5, b1 = (b / 5) % 5, b2 = b / 25;
+            double x = (double)theta[k][0] * (2 * b0 - 4) + (double)theta[k][1] * (2 * b1 - 4);
+            x = x + (double)theta[k][2] * (2 * b2 - 4);
+            P[b] = llrint(x * 65536.0);
+            idx[b] = b;
+        }
+        for (int a = 1; a < HIST_BINS; a++) { /* insertion sort by (P, b) */
+            int v = idx[a], m = a;
+            while (m > 0 && (P[idx[m - 1]] > P[v] || (P[idx[m - 1]] == P[v] && idx[m - 1] > v))) {
+                idx[m] = idx[m - 1];
+                m--;
+            }
+            idx[m] = v;
+        }
+        for (int r = 0; r < HIST_BINS; r++) perm[k][r] = (uint8_t)idx[r];
+        for (int r = 0; r + 1 < HIST_BINS; r++) gap[k][r] = P[idx[r + 1]] - P[idx[r]];
+    }
+}
+
+/* histogram of one cluster: Cholesky factor L of S = M / w (L L^T = S), samples
+ * normalize(L u_s), binned per component by floor((d + 1) * 2.5) clamped to [0, 4] */
+static void cluster_hist(const i128 acc[7], const float (*u)[3], int N, uint16_t H[HIST_BINS]) {
+    float wf = deq32(acc[0]);
+    float S[6];
+    for (int e = 0; e < 6; e++) S[e] = deq32(acc[1 + e]) / wf;
+    float L00 = sqrtf(fmaxf_(S[0], 0.0f));
+    float L10 = L00 > 0.0f ? S[3] / L00 : 0.0f;
+    float L20 = L00 > 0.0f ? S[4] / L00 : 0.0f;
+    float t = S[1] - L10 * L10;
+    float L11 = sqrtf(fmaxf_(t, 0.0f));
+    float L21 = L11 > 0.0f ? (S[5] - L20 * L10) / L11 : 0.0f;
+    t = (S[2] - L20 * L20) - L21 * L21;
+    float L22 = sqrtf(fmaxf_(t, 0.0f));
+    memset(H, 0, sizeof(uint16_t) * HIST_BINS);
+    for (int s = 0; s < N; s++) {
+        float v0 = L00 * u[s][0];
+        float v1 = L10 * u[s][0] + L11 * u[s][1];
+        float v2 = (L20 * u[s][0] + L21 * u[s][1]) + L22 * u[s][2];
+        float n2 = (v0 * v0 + v1 * v1) + v2 * v2;
+        int b[3] = {2, 2, 2};
+        if (n2 > 0.0f) {
+            float r = sqrtf(n2);
+            float inv = 1.0f / r;
+            float d[3] = {v0 * inv, v1 * inv, v2 * inv};
+            for (int c = 0; c < 3; c++) {
+                int bi = (int)floorf((d[c] + 1.0f) * 2.5f);
+                b[c] = bi < 0 ? 0 : (bi > 4 ? 4 : bi);
+            }
+        }
+        H[b[0] + 5 * b[1] + 25 * b[2]]++;
+    }
+}
+
+/* d_hist = sum over slices k of sum_r |C_r| * gap[k][r], C_r the running count difference */
+static int64_t hist_dist(const uint16_t* Hi, const uint16_t* Hj, const uint8_t perm[32][HIST_BINS],
+                         const int64_t gap[32][HIST_BINS - 1]) {
+    int64_t d = 0;
+    for (int k = 0; k < 32; k++) {
+        int64_t C = 0, W = 0;
+        for (int r = 0; r + 1 < HIST_BINS; r++) {
+            C += (int64_t)Hi[perm[k][r]] - (int64_t)Hj[perm[k][r]];
+            W += (C < 0 ? -C : C) * gap[k][r];
+        }
+        d += W;
+    }
+    return d;
+}
+
+
+static int hist_tables_init(hist_tables_t* T, int N) {
+    if (N < HIST_NMIN || N > HIST_NMAX) return ORC_ERR_ARG;
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    T->N = N;
+    T->u = (float(*)[3])malloc(sizeof(float) * 3 * N);
+    if (!T->u) return ORC_ERR_OOM;
+    sample_table(N, T->u);
+    sw_tables(theta, T->perm, T->gap);
+    return ORC_OK;
+}
+
+/* SGGX-H (§9) with d_hist; histograms are kept per cluster and redrawn for a merged one */
+static int sggxh_hist(i128 (*cl)[7], int n, int K, const hist_tables_t* T) {
+    uint16_t H[8 * MAX_K][HIST_BINS];
+    for (int c = 0; c < n; c++) cluster_hist(cl[c], (const float(*)[3])T->u, T->N, H[c]);
+    while (n > K) {
+        int bi = 0, bj = 1, have = 0;
+        int64_t best = 0;
+        for (int i = 0; i < n; i++)
+            for (int j = i + 1; j < n; j++) {
+                int64_t d = hist_dist(H[i], H[j], T->perm, T->gap);
+                if (!have || d < best) { best = d; bi = i; bj = j; have = 1; }
+            }
+        for (int e = 0; e < 7; e++) cl[bi][e] += cl[bj][e];
+        cluster_hist(cl[bi], (const float(*)[3])T->u, T->N, H[bi]);
+        for (int c = bj; c + 1 < n; c++) {
+            memcpy(cl[c], cl[c + 1], sizeof(cl[c]));
+            memcpy(H[c], H[c + 1], sizeof(H[c]));
+        }
+        n--;
+    }
+    return n;
+}
+
+void orc_sample_table(int N, float* out) { sample_table(N, (float(*)[3])out); }
+
+void orc_sw_tables(uint8_t* perm, int64_t* gap) {
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    sw_tables(theta, (uint8_t(*)[HIST_BINS])perm, (int64_t(*)[HIST_BINS - 1])gap);
+}
+
+int orc_hist(const int64_t acc[7], int N, uint16_t* H) {
+    hist_tables_t T;
+    int rc = hist_tables_init(&T, N);
+    if (rc != ORC_OK) return rc;
+    i128 a[7];
+    for (int e = 0; e < 7; e++) a[e] = acc[e];
+    cluster_hist(a, (const float(*)[3])T.u, N, H);
+    free(T.u);
+    return ORC_OK;
+}
+
+int64_t orc_hist_distance(const uint16_t* Hi, const uint16_t* Hj) {
+    float theta[32][3], coef[32][6];
+    uint8_t perm[32][HIST_BINS];
+    int64_t gap[32][HIST_BINS - 1];
+    theta_table(theta, coef);
+    sw_tables(theta, perm, gap);
+    return hist_dist(Hi, Hj, perm, gap);
+}
+
+int orc_sggxh_hist(int n, const int64_t* acc, int K, int N, int64_t* out) {
+    if (n < 0 || n > 8 * MAX_K || K < 1 || K > MAX_K) return ORC_ERR_ARG;
+    hist_tables_t T;
+    int rc = hist_tables_init(&T, N);
+    if (rc != ORC_OK) return rc;
+    i128 cl[8 * MAX_K][7];
+    int m = 0;
+    for (int c = 0; c < n; c++) {
+        if (acc[7 * c] == 0) continue;
+        for (int e = 0; e < 7; e++) cl[m][e] = acc[7 * c + e];
+        m++;
+    }
+    if (m > K) m = sggxh_hist(cl, m, K, &T);
+    free(T.u);
+    for (int c = 0; c < m; c++)
+        for (int e = 0; e < 7; e++) {
+            if (!fits64(cl[c][e])) return ORC_ERR_OVERFLOW;
+            out[7 * c + e] = (int64_t)cl[c][e];
+        }
+    return m;
+}
+
 static int cmp_rec(const void* x, const void* y) {
     uint64_t a = ((const rec_t*)x)->key, b = ((const rec_t*)y)->key;
     return a < b ? -1 : a > b;
@@ -763,7 +979,7 @@ int orc_build(orc_ctx* c, int levels) {
                 }
                 x++;
             }
-            if (n > K) n = sggxh(list, n, K, coef);
+            if (n > K) n = c->mode == 1 ? sggxh_hist(list, n, K, c->ht) : sggxh(list, n, K, coef);
             P->ncl[p] = (uint8_t)n;
             for (int q = 0; q < n; q++)
                 for (int e = 0; e < 7; e++) {
