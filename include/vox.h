@@ -53,6 +53,10 @@ typedef struct {
     uint32_t n_slices;     /* slice directions of the SGGX-H distance: 32 only (default 32) */
     uint64_t max_bytes;    /* cap on scratch+output device bytes per call (0 = no cap) */
     int profile;           /* 1 = record per-stage CUDA events (vox_stats times) */
+    int distance_mode;     /* SGGX-H distance: 0 = sigma (PREDICATES §9, default), 1 = the paper's
+                            * histogram distance (§10: N samples per SGGX, 5x5x5 bins, sliced W1;
+                            * P:383-389) */
+    uint32_t hist_samples; /* N of distance_mode 1, 32..8160 (0 = 5000) */
 } vox_options;
 
 /* Level view. Level 0 (leaves): ncl and cl are NULL; a leaf holds exactly one lobe
@@ -149,6 +153,12 @@ vox_status vox_plan_shards(const uint64_t* weights, uint64_t ncells, int world, 
 
 /* Host copy of the SGGX-H slice table (PREDICATES §9): theta [32][3], coef [32][6]. */
 vox_status vox_theta_table(float* theta, float* coef);
+
+/* Host copy of the histogram-distance tables (PREDICATES §10) for N samples (32..8160):
+ * u [3][N] whole-sphere sample table (SoA x, y, z), perm [124][32] the first 124 sorted
+ * cells of each slice (transposed: perm[r*32 + k]), gap [124][32] the fixed-point gaps.
+ * Any pointer may be NULL (not written). VOX_ERR_INVALID_ARG for N out of range. */
+vox_status vox_hist_tables(uint32_t N, float* u, uint8_t* perm, uint32_t* gap);
 
 vox_status vox_stats_get(vox_ctx* ctx, vox_stats* out);   /* synchronises the stream */
 vox_status vox_stats_reset(vox_ctx* ctx);

@@ -34,7 +34,8 @@ class VoxError(RuntimeError):
 
 class _Options(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int), ("top_depth", C.c_int),
-                ("k", C.c_uint32), ("n_slices", C.c_uint32), ("max_bytes", C.c_uint64), ("profile", C.c_int)]
+                ("k", C.c_uint32), ("n_slices", C.c_uint32), ("max_bytes", C.c_uint64), ("profile", C.c_int),
+                ("distance_mode", C.c_int), ("hist_samples", C.c_uint32)]
 
 
 class _View(C.Structure):
@@ -80,6 +81,7 @@ def lib():
     L.vox_import_level.argtypes = [vp, u32, vp, u64]
     L.vox_plan_shards.argtypes = [C.POINTER(u64), u64, i32, C.POINTER(u64)]
     L.vox_theta_table.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    L.vox_hist_tables.argtypes = [u32, vp, vp, vp]
     L.vox_stats_get.argtypes = [vp, C.POINTER(_Stats)]
     L.vox_stats_reset.argtypes = [vp]
     L.vox_sync.argtypes = [vp]
@@ -92,7 +94,7 @@ def lib():
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
                  "vox_copy_level", "vox_copy_level_acc", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
-                 "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
+                 "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
     _lib = L
     return L
@@ -122,6 +124,19 @@ def theta_table():
     return t, c
 
 
+def hist_tables(n: int = 5000):
+    """The library's histogram-distance tables (PREDICATES §10): u [3, n] (SoA sample table),
+    perm [124, 32] and gap [124, 32] (transposed slice tables)."""
+    u = np.zeros((3, n), np.float32)
+    perm = np.zeros((124, 32), np.uint8)
+    gap = np.zeros((124, 32), np.uint32)
+    rc = lib().vox_hist_tables(int(n), C.c_void_p(u.ctypes.data), C.c_void_p(perm.ctypes.data),
+                               C.c_void_p(gap.ctypes.data))
+    if rc != 0:
+        raise VoxError(rc, "vox_hist_tables")
+    return u, perm, gap
+
+
 def _dev_f32(t, name, shape_tail):
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
@@ -143,7 +158,8 @@ class Vox:
     """
 
     def __init__(self, grid_res: int, bbox, k: int = 3, rank: int = 0, world: int = 1, top_depth: int = 0,
-                 max_bytes: int = 0, profile: bool = False, stream=None):
+                 max_bytes: int = 0, profile: bool = False, stream=None, distance: str = "sigma",
+                 hist_samples: int = 5000):
         import torch
         self.grid_res = int(grid_res)
         self.k = int(k)
@@ -153,8 +169,11 @@ class Vox:
             stream = torch.cuda.current_stream()
         self.stream = stream
         bb = (C.c_float * 6)(*[float(x) for x in np.asarray(bbox, np.float32).reshape(6)])
+        if distance not in ("sigma", "hist"):
+            raise ValueError(f"distance must be 'sigma' or 'hist', not {distance!r}")
+        self.distance = distance
         opt = _Options(C.c_void_p(stream.cuda_stream), int(rank), int(world), int(top_depth), int(k), 32,
-                       int(max_bytes), int(bool(profile)))
+                       int(max_bytes), int(bool(profile)), 1 if distance == "hist" else 0, int(hist_samples))
         h = C.c_void_p()
         st = lib().vox_create(C.byref(h), self.grid_res, bb, C.byref(opt))
         if st:

@@ -1,0 +1,300 @@
+// SGGX-H with the paper's histogram distance (distance_mode = 1; docs/PREDICATES.md §10,
+// SURVEY §8(f) NEXT-1): N whole-sphere samples per SGGX, a 5x5x5 histogram
+// (P:389), the sliced Wasserstein-1 distance between histograms over the 32 slices of
+// §9, in exact integer arithmetic.
+//
+// One warp per parent with n > K (every level, leaves included). A lobe's histogram is built
+// by the whole warp: lane l takes samples l, l+32, ... of the sample table (SoA in global,
+// L1/L2-resident), bins them with the pinned fp32 sequence and counts into its own byte
+// column of a [125][32] shared-memory counter block (no atomics: N <= 8160 keeps a lane's
+// count <= 255); a dp4a pass sums the columns. A pair distance has lane k walk slice k's
+// 124 sorted bins (tables transposed [r][32] in shared memory, conflict-free) accumulating
+// |C| * gap in 64-bit integers; a xor-shuffle sum finishes it (exact, order-free).
+#include "vox_internal.cuh"
+
+#include <algorithm>
+#include <vector>
+
+namespace vox {
+
+constexpr int HB = 125;   // histogram cells
+constexpr int HR = 124;   // sorted gaps per slice
+
+// ---------------------------------------------------------------- host tables (§10)
+void host_hist_tables(int N, std::vector<float>& u, std::vector<uint8_t>& permT, std::vector<uint32_t>& gapT) {
+    const double pi = 3.14159265358979323846;
+    const double golden_angle = pi * (3.0 - std::sqrt(5.0));
+    u.assign(3 * (size_t)N, 0.0f);
+    for (int s = 0; s < N; s++) {
+        const double z = 1.0 - (2.0 * s + 1.0) / N;
+        const double rho = std::sqrt(1.0 - z * z);
+        const double phi = s * golden_angle;
+        u[s] = (float)(rho * std::cos(phi));
+        u[N + s] = (float)(rho * std::sin(phi));
+        u[2 * (size_t)N + s] = (float)z;
+    }
+    float theta[32][3], coef[32][6];
+    host_theta(theta, coef);
+    permT.assign(HR * 32, 0);
+    gapT.assign(HR * 32, 0);
+    for (int k = 0; k < 32; k++) {
+        long long P[HB];
+        int idx[HB];
+        for (int b = 0; b < HB; b++) {
+            const int b0 = b % 5, b1 = (b / 5) % 5, b2 = b / 25;
+            double x = (double)theta[k][0] * (2 * b0 - 4) + (double)theta[k][1] * (2 * b1 - 4);
+            x = x + (double)theta[k][2] * (2 * b2 - 4);
+            P[b] = std::llrint(x * 65536.0);
+            idx[b] = b;
+        }
+        std::stable_sort(idx, idx + HB, [&](int a, int b) { return P[a] < P[b]; });
+        for (int r = 0; r < HR; r++) {
+            permT[r * 32 + k] = (uint8_t)idx[r];
+            gapT[r * 32 + k] = (uint32_t)(P[idx[r + 1]] - P[idx[r]]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- device pieces
+__device__ __forceinline__ int hist_bin1(float d) {
+    const int b = (int)floorf((d + 1.0f) * 2.5f);
+    return b < 0 ? 0 : (b > 4 ? 4 : b);
+}
+
+// histogram of the lobe (w, M6) accumulators `lob` into H[0..124]; priv: 1000 words scratch
+__device__ __forceinline__ void hist_build(const long long* lob, const float* __restrict__ ux,
+                                           const float* __restrict__ uy, const float* __restrict__ uz, int N,
+                                           uint32_t* priv, uint16_t* H, int lane) {
+    for (int w = lane; w < HB * 8; w += 32) priv[w] = 0u;
+    const float wf = deq32(lob[0]);
+    float S[6];
+#pragma unroll
+    for (int e = 0; e < 6; e++) S[e] = deq32(lob[1 + e]) / wf;
+    const float L00 = sqrtf(pmax(S[0], 0.0f));
+    const float L10 = L00 > 0.0f ? S[3] / L00 : 0.0f;
+    const float L20 = L00 > 0.0f ? S[4] / L00 : 0.0f;
+    const float L11 = sqrtf(pmax(S[1] - L10 * L10, 0.0f));
+    const float L21 = L11 > 0.0f ? (S[5] - L20 * L10) / L11 : 0.0f;
+    const float L22 = sqrtf(pmax((S[2] - L20 * L20) - L21 * L21, 0.0f));
+    __syncwarp();
+    uint8_t* pb = reinterpret_cast<uint8_t*>(priv);
+    for (int s = lane; s < N; s += 32) {
+        const float u0 = ux[s], u1 = uy[s], u2 = uz[s];
+        const float v0 = L00 * u0;
+        const float v1 = L10 * u0 + L11 * u1;
+        const float v2 = (L20 * u0 + L21 * u1) + L22 * u2;
+        const float n2 = (v0 * v0 + v1 * v1) + v2 * v2;
+        int b = 62;   // cell (2,2,2) when v = 0
+        if (n2 > 0.0f) {
+            const float r = sqrtf(n2);
+            const float inv = 1.0f / r;
+            b = hist_bin1(v0 * inv) + 5 * hist_bin1(v1 * inv) + 25 * hist_bin1(v2 * inv);
+        }
+        pb[b * 32 + lane] += 1;
+    }
+    __syncwarp();
+    for (int b = lane; b < HB; b += 32) {
+        unsigned sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) sum = __dp4a(priv[b * 8 + q], 0x01010101u, sum);
+        H[b] = (uint16_t)sum;
+    }
+    __syncwarp();
+}
+
+// d_hist(i, j) (PREDICATES §10): lane k walks slice k; exact 64-bit warp sum
+__device__ __forceinline__ unsigned long long hist_pair(const uint16_t* Hi, const uint16_t* Hj,
+                                                        const uint8_t* permT, const uint32_t* gapT, int lane) {
+    int C = 0;
+    unsigned long long W = 0;
+#pragma unroll 4
+    for (int r = 0; r < HR; r++) {
+        const int b = permT[r * 32 + lane];
+        C += (int)Hi[b] - (int)Hj[b];
+        W += (unsigned long long)(unsigned)(C < 0 ? -C : C) * gapT[r * 32 + lane];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+    return W;
+}
+
+// key = (d << 16) | (i << 8) | j orders by (d, i, j); d < 2^38 (32 slices x N x 2^20)
+__device__ __forceinline__ unsigned long long hist_key(unsigned long long d, int i, int j) {
+    return (d << 16) | (unsigned long long)((i << 8) | j);
+}
+constexpr unsigned long long HIST_RETIRED = 0xFFFFFFFFFFFFull << 16;
+
+template <int K>
+struct HistSmem {
+    static constexpr int MAXN = 8 * K;
+    static constexpr int MAXP = MAXN * (MAXN - 1) / 2;
+    static constexpr int WARPS = K <= 4 ? 4 : 2;
+    static constexpr size_t tables = HR * 32 + HR * 32 * 4;                  // perm u8 + gap u32
+    static constexpr size_t lob_bytes = MAXN * 7 * 8;
+    static constexpr size_t H_bytes = MAXN * 128 * 2;
+    static constexpr size_t priv_bytes = HB * 32;
+    static constexpr size_t D_bytes = ((MAXP * 8 + 15) / 16) * 16;
+    static constexpr size_t per_warp = lob_bytes + H_bytes + priv_bytes + D_bytes;
+    static constexpr size_t total = tables + WARPS * per_warp;
+};
+
+template <int K>
+__global__ void __launch_bounds__(128)
+k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
+             const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
+             const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
+             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+             const float* __restrict__ hu, int N, const uint8_t* __restrict__ gperm,
+             const uint32_t* __restrict__ ggap) {
+    using SM = HistSmem<K>;
+    constexpr int MAXN = SM::MAXN;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint8_t* permT = smem_raw;
+    uint32_t* gapT = reinterpret_cast<uint32_t*>(smem_raw + HR * 32);
+    for (int x = threadIdx.x; x < HR * 8; x += blockDim.x)
+        reinterpret_cast<uint32_t*>(permT)[x] = reinterpret_cast<const uint32_t*>(gperm)[x];
+    for (int x = threadIdx.x; x < HR * 32; x += blockDim.x) gapT[x] = ggap[x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* base = smem_raw + SM::tables + wib * SM::per_warp;
+    long long(*lob)[7] = reinterpret_cast<long long(*)[7]>(base);
+    uint16_t(*H)[128] = reinterpret_cast<uint16_t(*)[128]>(base + SM::lob_bytes);
+    uint32_t* priv = reinterpret_cast<uint32_t*>(base + SM::lob_bytes + SM::H_bytes);
+    unsigned long long* D = reinterpret_cast<unsigned long long*>(base + SM::lob_bytes + SM::H_bytes + SM::priv_bytes);
+    const float *ux = hu, *uy = hu + N, *uz = hu + 2 * N;
+    const unsigned hi = counts[2];
+    for (unsigned w = blockIdx.x * SM::WARPS + wib; w < hi; w += gridDim.x * SM::WARPS) {
+        const uint64_t p = list[w];
+        const uint32_t c0 = start[p], c1 = start[p + 1];
+        int n = 0;
+        // dendrogram leaves in child-slot order, w = 0 dropped (D17)
+        if (leaf) {
+            const int nch = (int)(c1 - c0);
+            const bool has = lane < nch && cacc[7 * (uint64_t)(c0 + lane)] > 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, has);
+            n = __popc(bal);
+            if (has) {
+                const int c = __popc(bal & ((1u << lane) - 1u));
+#pragma unroll
+                for (int e = 0; e < 7; e++) lob[c][e] = cacc[7 * (uint64_t)(c0 + lane) + e];
+            }
+        } else {
+            const int slots = (int)(c1 - c0) * K;
+            for (int b = 0; b < 8 * K; b += 32) {
+                const int sl = b + lane;
+                bool has = false;
+                const long long* src = nullptr;
+                if (sl < slots) {
+                    const uint64_t x = c0 + sl / K;
+                    const int q = sl % K;
+                    src = cclacc + (x * K + q) * 7;
+                    has = q < cncl[x] && src[0] != 0;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, has);
+                if (has) {
+                    const int c = n + __popc(bal & ((1u << lane) - 1u));
+#pragma unroll
+                    for (int e = 0; e < 7; e++) lob[c][e] = src[e];
+                }
+                n += __popc(bal);
+            }
+        }
+        __syncwarp();
+        for (int c = 0; c < n; c++) hist_build(lob[c], ux, uy, uz, N, priv, H[c], lane);
+        for (int j = 1, t = 0; j < n; j++)
+            for (int i = 0; i < j; i++, t++) {
+                const unsigned long long d = hist_pair(H[i], H[j], permT, gapT, lane);
+                if (lane == 0) D[t] = hist_key(d, i, j);
+            }
+        __syncwarp();
+        const int np = n * (n - 1) / 2;
+        unsigned long long alive = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+        for (int m = n; m > K; m--) {
+            unsigned long long best = ~0ull;
+            for (int t = lane; t < np; t += 32) {
+                const unsigned long long key = D[t];
+                best = key < best ? key : best;
+            }
+            const unsigned bh = (unsigned)(best >> 32);
+            const unsigned dmin = __reduce_min_sync(0xffffffffu, bh);
+            const unsigned lmin = __reduce_min_sync(0xffffffffu, bh == dmin ? (unsigned)best : 0xffffffffu);
+            const int bi = (int)((lmin >> 8) & 0xff), bj = (int)(lmin & 0xff);
+            if (lane < 7) lob[bi][lane] += lob[bj][lane];   // exact moment merge (D15)
+            alive &= ~(1ull << bj);
+            __syncwarp();
+            hist_build(lob[bi], ux, uy, uz, N, priv, H[bi], lane);   // fresh histogram of the merged S
+            for (int x = 0; x < n; x++) {
+                if (x == bi || !((alive >> x) & 1ull)) continue;
+                const unsigned long long d = hist_pair(H[bi], H[x], permT, gapT, lane);
+                const int a = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                if (lane == 0) D[b2 * (b2 - 1) / 2 + a] = hist_key(d, a, b2);
+            }
+            for (int x = lane; x < n; x += 32)
+                if (x != bj) {
+                    const int a = x < bj ? x : bj, b2 = x < bj ? bj : x;
+                    D[b2 * (b2 - 1) / 2 + a] = HIST_RETIRED | (unsigned long long)((a << 8) | b2);
+                }
+            __syncwarp();
+        }
+        int slot = 0;
+        for (int cc = 0; cc < n; cc++) {
+            if (!((alive >> cc) & 1ull)) continue;
+            if (lane < 7) {
+                const long long a = lob[cc][lane];
+                pclacc[(p * K + slot) * 7 + lane] = a;
+                pcl[(p * K + slot) * 7 + lane] = deq32(a);
+            }
+            slot++;
+        }
+        if (lane == 0) pncl[p] = (uint8_t)slot;
+        __syncwarp();
+        (void)MAXN;
+    }
+}
+
+template <int K>
+static cudaError_t launch_hist_k(vox_ctx* c, const uint32_t* list, const unsigned* counts, const Level& C, int leaf,
+                                 const uint32_t* start, Level& P) {
+    using SM = HistSmem<K>;
+    cudaError_t e = cudaFuncSetAttribute(k_sggxh_hist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SM::total);
+    if (e != cudaSuccess) return e;
+    uint64_t nb = (P.n + SM::WARPS - 1) / SM::WARPS;
+    nb = std::min<uint64_t>(std::max<uint64_t>(nb, 1), 148ull * 8);
+    k_sggxh_hist<K><<<(unsigned)nb, SM::WARPS * 32, SM::total, c->stream>>>(
+        list, counts, C.acc, C.ncl, C.clacc, leaf, start, P.ncl, P.clacc, P.cl, c->d_hist_u, c->hist_n,
+        c->d_hist_perm, c->d_hist_gap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
+                              int leaf, const uint32_t* start, Level& P) {
+    switch (K) {
+        case 1: return launch_hist_k<1>(c, list, counts, C, leaf, start, P);
+        case 2: return launch_hist_k<2>(c, list, counts, C, leaf, start, P);
+        case 3: return launch_hist_k<3>(c, list, counts, C, leaf, start, P);
+        case 4: return launch_hist_k<4>(c, list, counts, C, leaf, start, P);
+        case 5: return launch_hist_k<5>(c, list, counts, C, leaf, start, P);
+        case 6: return launch_hist_k<6>(c, list, counts, C, leaf, start, P);
+        case 7: return launch_hist_k<7>(c, list, counts, C, leaf, start, P);
+        default: return launch_hist_k<8>(c, list, counts, C, leaf, start, P);
+    }
+}
+
+cudaError_t upload_hist_tables(vox_ctx* c) {
+    if (c->d_hist_u) return cudaSuccess;
+    std::vector<float> u;
+    std::vector<uint8_t> perm;
+    std::vector<uint32_t> gap;
+    host_hist_tables(c->hist_n, u, perm, gap);
+    cudaError_t e;
+    if ((e = cudaMalloc((void**)&c->d_hist_u, u.size() * 4)) != cudaSuccess) return e;
+    if ((e = cudaMalloc((void**)&c->d_hist_perm, perm.size())) != cudaSuccess) return e;
+    if ((e = cudaMalloc((void**)&c->d_hist_gap, gap.size() * 4)) != cudaSuccess) return e;
+    // synchronous copies from pageable host vectors (once per ctx)
+    if ((e = cudaMemcpy(c->d_hist_u, u.data(), u.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(c->d_hist_perm, perm.data(), perm.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    return cudaMemcpy(c->d_hist_gap, gap.data(), gap.size() * 4, cudaMemcpyHostToDevice);
+}
+
+}  // namespace vox

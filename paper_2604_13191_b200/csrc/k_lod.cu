@@ -995,6 +995,12 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     k_bucket_scatter<<<(unsigned)(sb ? sb : 1), 256, 0, c->stream>>>(nlob, V, K, MAXN, cursor, list);
     c->st.launches += 3;
     // grids cover the worst case (every parent hard); blocks stride over the actual counts
+    if (c->dmode == 1) {   // histogram distance (§10): one kernel for every n > K
+        timer_begin(c, c->t_warp);
+        CK(launch_sggxh_hist(c, K, list, counts, C, leaf, start, P));
+        timer_end(c, c->t_warp);
+        c->st.launches++;
+    } else {
     if (K < 8) {
         uint64_t qb = ((V + 3) / 4 + QUAD_WARPS - 1) / QUAD_WARPS;
         qb = std::min<uint64_t>(std::max<uint64_t>(qb, 1), 148ull * 48);
@@ -1025,6 +1031,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
                                                                           P.ncl, P.clacc, P.cl);
         timer_end(c, c->t_warp);
         c->st.launches++;
+    }
     }
     CK(cudaGetLastError());
     dfree(c, list);

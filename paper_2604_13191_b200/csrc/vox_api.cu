@@ -183,6 +183,7 @@ static vox_status ensure_dev(vox_ctx* c) {
     CKS(cudaMallocAsync((void**)&c->d_lodwork, 32, c->stream));
     CKS(cudaMemsetAsync(c->d_lodwork, 0, 32, c->stream));
     upload_theta(c);
+    if (c->dmode == 1) CKS(upload_hist_tables(c));
     CKS(cudaGetLastError());
     return VOX_OK;
 }
@@ -227,6 +228,9 @@ vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], con
     if (o.k == 0) o.k = 3;
     if (o.k > VOX_MAX_K) return VOX_ERR_INVALID_ARG;
     if (o.n_slices != 0 && o.n_slices != VOX_SLICES) return VOX_ERR_INVALID_ARG;
+    if (o.distance_mode < 0 || o.distance_mode > 1) return VOX_ERR_INVALID_ARG;
+    if (o.hist_samples == 0) o.hist_samples = 5000;
+    if (o.hist_samples < 32 || o.hist_samples > 8160) return VOX_ERR_INVALID_ARG;
     vox_ctx* c = new (std::nothrow) vox_ctx();
     if (!c) return VOX_ERR_OOM;
     for (int a = 0; a < 3; a++) c->g.bmin[a] = bbox[a];
@@ -241,6 +245,8 @@ vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], con
     c->K = o.k;
     c->max_bytes = o.max_bytes;
     c->profile = o.profile;
+    c->dmode = o.distance_mode;
+    c->hist_n = (int)o.hist_samples;
     c->built = 0;
     c->st.top_depth = (uint32_t)c->T;
     *out = c;
@@ -589,6 +595,18 @@ vox_status vox_theta_table(float* theta, float* coef) {
     return VOX_OK;
 }
 
+vox_status vox_hist_tables(uint32_t N, float* u, uint8_t* perm, uint32_t* gap) {
+    if (N < 32 || N > 8160) return VOX_ERR_INVALID_ARG;
+    std::vector<float> hu;
+    std::vector<uint8_t> hp;
+    std::vector<uint32_t> hg;
+    host_hist_tables((int)N, hu, hp, hg);
+    if (u) std::memcpy(u, hu.data(), hu.size() * sizeof(float));
+    if (perm) std::memcpy(perm, hp.data(), hp.size());
+    if (gap) std::memcpy(gap, hg.data(), hg.size() * sizeof(uint32_t));
+    return VOX_OK;
+}
+
 vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     if (!c || !out) return VOX_ERR_INVALID_ARG;
     CKS(ssync(c));
@@ -659,6 +677,9 @@ void vox_destroy(vox_ctx* c) {
     }
     c->ev_pool.clear();
     if (c->d_lodwork) cudaFreeAsync(c->d_lodwork, c->stream);
+    if (c->d_hist_u) cudaFree(c->d_hist_u);
+    if (c->d_hist_perm) cudaFree(c->d_hist_perm);
+    if (c->d_hist_gap) cudaFree(c->d_hist_gap);
     if (c->d_flags) cudaFreeAsync(c->d_flags, c->stream);
     if (c->d_counter) cudaFreeAsync(c->d_counter, c->stream);
     ssync(c);

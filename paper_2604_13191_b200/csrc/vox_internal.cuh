@@ -158,6 +158,11 @@ struct vox_ctx {
     unsigned long long* d_counter = nullptr; // pair cursor
     vox_stats st{};
     std::string err;
+    int dmode = 0;                          // 0 sigma distance, 1 histogram distance (§10)
+    int hist_n = 5000;                      // samples per histogram (§10)
+    float* d_hist_u = nullptr;              // [3][N] sample table (SoA)
+    uint8_t* d_hist_perm = nullptr;         // [124][32] sorted bins per slice (transposed)
+    uint32_t* d_hist_gap = nullptr;         // [124][32] fixed-point gaps (transposed)
     // stage timers (profile = 1)
     vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp;
 };
@@ -195,6 +200,11 @@ vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigne
 // LoD (k_lod.cu)
 vox_status build_level(vox_ctx* c, int l);
 void upload_theta(vox_ctx* c);
+// histogram distance (k_hist.cu)
+void host_hist_tables(int N, std::vector<float>& u, std::vector<uint8_t>& permT, std::vector<uint32_t>& gapT);
+cudaError_t upload_hist_tables(vox_ctx* c);
+cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
+                              int leaf, const uint32_t* start, Level& P);
 void host_theta(float theta[32][3], float coef[32][6]);
 // fp32 outputs of a level from its accumulators (k_lod.cu)
 cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters);

@@ -30,6 +30,17 @@ def test_exports_every_declared_symbol(P):
         assert hasattr(L, n), n
 
 
+def test_hist_tables_bit_identical_to_oracle(P):
+    for n in (32, 5000, 8160):
+        u1, perm1, gap1 = P.hist_tables(n)
+        assert np.array_equal(u1.T.view(np.uint32), oracle.sample_table(n).view(np.uint32))
+    perm2, gap2 = oracle.sw_tables()
+    assert np.array_equal(perm1.T, perm2[:, :124])
+    assert np.array_equal(gap1.T.astype(np.int64), gap2)
+    with pytest.raises(P.VoxError):
+        P.hist_tables(31)
+
+
 def test_theta_table_bit_identical_to_oracle(P):
     t1, c1 = P.theta_table()
     t2, c2 = oracle.theta()
