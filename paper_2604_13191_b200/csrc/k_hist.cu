@@ -78,8 +78,7 @@ __device__ __forceinline__ void hist_build(const long long* lob, const float* __
     const float L22 = sqrtf(pmax((S[2] - L20 * L20) - L21 * L21, 0.0f));
     __syncwarp();
     uint8_t* pb = reinterpret_cast<uint8_t*>(priv);
-    for (int s = lane; s < N; s += 32) {
-        const float u0 = ux[s], u1 = uy[s], u2 = uz[s];
+    auto bin_uv = [&](float u0, float u1, float u2) {
         const float v0 = L00 * u0;
         const float v1 = L10 * u0 + L11 * u1;
         const float v2 = (L20 * u0 + L21 * u1) + L22 * u2;
@@ -90,8 +89,41 @@ __device__ __forceinline__ void hist_build(const long long* lob, const float* __
             const float inv = 1.0f / r;
             b = hist_bin1(v0 * inv) + 5 * hist_bin1(v1 * inv) + 25 * hist_bin1(v2 * inv);
         }
-        pb[b * 32 + lane] += 1;
+        return b;
+    };
+    auto bin_of = [&](int s) { return bin_uv(ux[s], uy[s], uz[s]); };
+    // four independent samples per step (ILP), the next step's table loads issued before this
+    // step's arithmetic (software pipelining); the counter updates follow in sample order
+    int s = lane;
+    if (s + 96 < N) {
+        float a[12];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            a[3 * q] = ux[s + 32 * q];
+            a[3 * q + 1] = uy[s + 32 * q];
+            a[3 * q + 2] = uz[s + 32 * q];
+        }
+        for (; s + 96 < N; s += 128) {
+            float c[12];
+#pragma unroll
+            for (int q = 0; q < 12; q++) c[q] = a[q];
+            if (s + 128 + 96 < N) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    a[3 * q] = ux[s + 128 + 32 * q];
+                    a[3 * q + 1] = uy[s + 128 + 32 * q];
+                    a[3 * q + 2] = uz[s + 128 + 32 * q];
+                }
+            }
+            const int b0 = bin_uv(c[0], c[1], c[2]), b1 = bin_uv(c[3], c[4], c[5]);
+            const int b2 = bin_uv(c[6], c[7], c[8]), b3 = bin_uv(c[9], c[10], c[11]);
+            pb[b0 * 32 + lane] += 1;
+            pb[b1 * 32 + lane] += 1;
+            pb[b2 * 32 + lane] += 1;
+            pb[b3 * 32 + lane] += 1;
+        }
     }
+    for (; s < N; s += 32) pb[bin_of(s) * 32 + lane] += 1;
     __syncwarp();
     for (int b = lane; b < HB; b += 32) {
         unsigned sum = 0;
@@ -102,20 +134,46 @@ __device__ __forceinline__ void hist_build(const long long* lob, const float* __
     __syncwarp();
 }
 
-// d_hist(i, j) (PREDICATES §10): lane k walks slice k; exact 64-bit warp sum
-__device__ __forceinline__ unsigned long long hist_pair(const uint16_t* Hi, const uint16_t* Hj,
-                                                        const uint8_t* permT, const uint32_t* gapT, int lane) {
-    int C = 0;
-    unsigned long long W = 0;
-#pragma unroll 4
+// d_hist(i, j_q) for up to 4 rows j_q at once (PREDICATES §10): lane k walks slice k, the
+// table and H_i loads shared by the rows; exact 64-bit warp sums
+template <int R>
+__device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* const (&Hj)[4], const uint8_t* permT,
+                                           const uint32_t* gapT, int lane, unsigned long long (&out)[4]) {
+    int C[R];
+    unsigned long long W[R];
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+        C[q] = 0;
+        W[q] = 0;
+    }
+#pragma unroll 2
     for (int r = 0; r < HR; r++) {
         const int b = permT[r * 32 + lane];
-        C += (int)Hi[b] - (int)Hj[b];
-        W += (unsigned long long)(unsigned)(C < 0 ? -C : C) * gapT[r * 32 + lane];
+        const unsigned g = gapT[r * 32 + lane];
+        const int hi = Hi[b];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            C[q] += hi - (int)Hj[q][b];
+            W[q] += (unsigned long long)(unsigned)(C[q] < 0 ? -C[q] : C[q]) * g;
+        }
     }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
-    return W;
+    for (int q = 0; q < R; q++) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) W[q] += __shfl_xor_sync(0xffffffffu, W[q], o);
+        out[q] = W[q];
+    }
+}
+
+// distances of row i to the listed columns xs[0..m-1] (m <= 4), batched
+__device__ __forceinline__ void hist_row4(const uint16_t (*H)[128], int i, const int (&xs)[4], int m,
+                                          const uint8_t* permT, const uint32_t* gapT, int lane,
+                                          unsigned long long (&out)[4]) {
+    const uint16_t* Hj[4] = {H[xs[0]], H[xs[m > 1 ? 1 : 0]], H[xs[m > 2 ? 2 : 0]], H[xs[m > 3 ? 3 : 0]]};
+    if (m == 4) hist_pairs<4>(H[i], Hj, permT, gapT, lane, out);
+    else if (m == 3) hist_pairs<3>(H[i], Hj, permT, gapT, lane, out);
+    else if (m == 2) hist_pairs<2>(H[i], Hj, permT, gapT, lane, out);
+    else hist_pairs<1>(H[i], Hj, permT, gapT, lane, out);
 }
 
 // key = (d << 16) | (i << 8) | j orders by (d, i, j); d < 2^38 (32 slices x N x 2^20)
@@ -139,7 +197,7 @@ struct HistSmem {
 };
 
 template <int K>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 1)
 k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
@@ -201,10 +259,18 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         }
         __syncwarp();
         for (int c = 0; c < n; c++) hist_build(lob[c], ux, uy, uz, N, priv, H[c], lane);
-        for (int j = 1, t = 0; j < n; j++)
-            for (int i = 0; i < j; i++, t++) {
-                const unsigned long long d = hist_pair(H[i], H[j], permT, gapT, lane);
-                if (lane == 0) D[t] = hist_key(d, i, j);
+        // initial matrix: row i against columns j > i, four at a time
+        for (int i = 0; i + 1 < n; i++)
+            for (int j0 = i + 1; j0 < n; j0 += 4) {
+                const int m = n - j0 < 4 ? n - j0 : 4;
+                const int xs[4] = {j0, j0 + 1, j0 + 2, j0 + 3};
+                unsigned long long d[4];
+                hist_row4(H, i, xs, m, permT, gapT, lane, d);
+                if (lane < m) {
+                    const int j = j0 + lane;
+                    const unsigned long long dv = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
+                    D[j * (j - 1) / 2 + i] = hist_key(dv, i, j);
+                }
             }
         __syncwarp();
         const int np = n * (n - 1) / 2;
@@ -223,11 +289,26 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             alive &= ~(1ull << bj);
             __syncwarp();
             hist_build(lob[bi], ux, uy, uz, N, priv, H[bi], lane);   // fresh histogram of the merged S
-            for (int x = 0; x < n; x++) {
-                if (x == bi || !((alive >> x) & 1ull)) continue;
-                const unsigned long long d = hist_pair(H[bi], H[x], permT, gapT, lane);
-                const int a = x < bi ? x : bi, b2 = x < bi ? bi : x;
-                if (lane == 0) D[b2 * (b2 - 1) / 2 + a] = hist_key(d, a, b2);
+            {   // new row d(bi, x) for the live x, four at a time
+                unsigned long long rest = alive & ~(1ull << bi);
+                while (rest) {
+                    int xs[4] = {0, 0, 0, 0}, m = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (rest) {
+                            xs[q] = __ffsll((long long)rest) - 1;
+                            rest &= rest - 1;
+                            m++;
+                        }
+                    unsigned long long d[4];
+                    hist_row4(H, bi, xs, m, permT, gapT, lane, d);
+                    if (lane < m) {
+                        const int x = lane == 0 ? xs[0] : lane == 1 ? xs[1] : lane == 2 ? xs[2] : xs[3];
+                        const unsigned long long dv = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
+                        const int a = x < bi ? x : bi, b2 = x < bi ? bi : x;
+                        D[b2 * (b2 - 1) / 2 + a] = hist_key(dv, a, b2);
+                    }
+                }
             }
             for (int x = lane; x < n; x += 32)
                 if (x != bj) {

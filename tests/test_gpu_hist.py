@@ -58,8 +58,8 @@ def test_hist_config1_all_levels(P):
 
 @pytest.mark.parametrize("k,n", [(1, 5000), (2, 32), (3, 8160), (5, 1000), (8, 5000)])
 def test_hist_weave_k_and_n(P, k, n):
-    s, r = gen.plain_weave(n_warp=16, n_weft=16, n_seg=32, pitch=1 / 16)
-    v, o = _run(P, 128, np.array([0, 0, -0.1, 1, 1, 0.1], np.float32), 5, segs=s, radii=r, k=k, n=n)
+    s, r = gen.plain_weave(n_warp=8, n_weft=8, n_seg=16, pitch=1 / 8)
+    v, o = _run(P, 64, np.array([0, 0, -0.1, 1, 1, 0.1], np.float32), 5, segs=s, radii=r, k=k, n=n)
     _cmp(v, o, 5, f"weave k={k} n={n}")
 
 
