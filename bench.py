@@ -107,7 +107,7 @@ def _cells_by_count(seg, bbox, N, level):
     return u[order], cnt[order]
 
 
-def oracle_sample(c, target_segments: int, level: int):
+def oracle_sample(c, target_segments: int, level: int, distance: str = "sigma", hist_samples: int = 5000):
     """Time the oracle (single-threaded, as it stands) on whole Morton cells at `level`,
     largest first, until `target_segments` segments have been processed: every segment
     touching a cell is voxelized (its S_p needs all its keys) and the LoD is built inside the
@@ -125,7 +125,7 @@ def oracle_sample(c, target_segments: int, level: int):
         box_hi = box_lo + ((1 << level) + 4) * E / N
         sel = np.all((hi >= box_lo) & (lo <= box_hi), axis=1)
         s, r = np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
-        o = oracle.Oracle(N, bbox)
+        o = oracle.Oracle(N, bbox, distance=distance, hist_samples=hist_samples)
         o.set_window(level, int(cell))
         t0 = time.perf_counter()
         o.add_fibers(s, r)
@@ -136,7 +136,7 @@ def oracle_sample(c, target_segments: int, level: int):
         o.close()
         if done >= target_segments:
             break
-    desc = (f"oracle (plain C, 1 thread) on {len(used)} Morton cell(s) at level {level} "
+    desc = (f"oracle (plain C, 1 thread, {distance} distance) on {len(used)} Morton cell(s) at level {level} "
             f"({1 << level}^3 voxels each): {done} segments touching them voxelized + LoD levels 1..{level} "
             f"inside them")
     return done, secs, desc
@@ -171,6 +171,9 @@ def main():
     ap.add_argument("--segments", type=int, default=None, help="override the segment count (config 4/5)")
     ap.add_argument("--grid", type=int, default=None, help="grid resolution of a config-5 sweep point")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--distance", default="sigma", choices=["sigma", "hist"],
+                    help="SGGX-H distance: sigma (PREDICATES §9) or the paper's histogram distance (§10)")
+    ap.add_argument("--hist-samples", type=int, default=5000, help="N samples per SGGX histogram (P:389)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-segments", type=int, default=400_000, help="oracle sample size (cpu_baseline)")
@@ -207,7 +210,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(profile=False):
-        v = Vox(N, bbox, rank=rank, world=world, profile=profile)
+        v = Vox(N, bbox, rank=rank, world=world, profile=profile, distance=args.distance,
+                hist_samples=args.hist_samples)
         if fib:
             v.voxelize_fibers(d_a, d_b)
         else:
@@ -275,12 +279,18 @@ def main():
     flops_sggxh = 416.0 * sig_ev + 95.0 * dist_ev      # PREDICATES §9: 32 x 13 per sigma, 32+32+31 per distance
     kern = {
         ("k_fiber_emit" if fib else "k_tri_emit"): (stage["ms_emit"], "hbm", 28 * n_prims + 16 * P + 16 * n_prims),
-        "radix_sort(pairs)": (stage["ms_sort"], "hbm", 32 * P),
-        "segmented_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
+        "k_bin_count": (stage["ms_sort"], "hbm", 8 * P),
+        "k_bin_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
         "k_lod_prep": (stage["ms_lod_prep"], "hbm", bytes_lod),
-        "k_sggxh_quad+half+warp": (stage["ms_sggxh_quad"] + stage["ms_sggxh_half"] + stage["ms_sggxh_warp"], "alu",
-                                   flops_sggxh),
     }
+    if args.distance == "hist":
+        # PREDICATES §10: ~25 fp32 ops per sample (L u, |v|^2, sqrt, 1/r, 3 x (scale, +1, x2.5)), 4 integer
+        # ops per slice step of a distance (sub/add, abs, multiply, add), 32 x 124 steps per distance
+        flops_hist = 25.0 * sig_ev * args.hist_samples + 4.0 * 32 * 124 * dist_ev
+        kern["k_sggxh_hist"] = (stage["ms_sggxh_warp"], "alu", flops_hist)
+    else:
+        kern["k_sggxh_quad+half+warp"] = (stage["ms_sggxh_quad"] + stage["ms_sggxh_half"] + stage["ms_sggxh_warp"],
+                                          "alu", flops_sggxh)
     dom = max(kern, key=lambda k: kern[k][0])
     def roof_of(name):
         ms_k, bound, work = kern[name]
@@ -307,6 +317,8 @@ def main():
             "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config]
                        + (f" [point: {n_prims} segments at {N}^3]" if args.config == 5 else ""),
                        "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
+                       "sggxh_distance": args.distance if args.distance == "sigma"
+                       else f"hist (N={args.hist_samples} samples, 5x5x5 bins, sliced W1)",
                        "l2": "inputs (28 B x prims) larger than L2; no flush"},
             "lod_ms": stage["ms_total_lod"], "vox_ms": stage["ms_total_vox"],
             "hbm_alg_gbs_full_build": (bytes_vox + bytes_lod) / (ms_step / 1e3) / 1e9,
@@ -323,7 +335,7 @@ def main():
         host = {}
 
         def e2e_step():
-            v = Vox(N, bbox, rank=rank, world=world)
+            v = Vox(N, bbox, rank=rank, world=world, distance=args.distance, hist_samples=args.hist_samples)
             if fib:
                 v.voxelize_fibers_host(pa, pb)
             else:
@@ -368,7 +380,8 @@ def main():
     # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu_baseline and fib:
         lvl = 9 if N >= 4096 else max(1, int(math.log2(N)) - 3)
-        n, dt, desc = oracle_sample(c, args.cpu_segments, lvl)
+        target = args.cpu_segments if args.distance == "sigma" else max(1000, args.cpu_segments // 100)
+        n, dt, desc = oracle_sample(c, target, lvl, args.distance, args.hist_samples)
         line["cpu_baseline"] = {"value": n / dt, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc,
                                 "seconds": dt}
     if rank == 0:

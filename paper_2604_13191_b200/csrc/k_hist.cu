@@ -13,6 +13,8 @@
 #include "vox_internal.cuh"
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 namespace vox {
@@ -362,20 +364,42 @@ cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const uns
     }
 }
 
+// Device tables are built once per (device, N) and kept for the process (like the event
+// pool): creating a ctx in the histogram mode costs no host table work or copies after that.
+struct HistTablesDev {
+    float* u = nullptr;
+    uint8_t* perm = nullptr;
+    uint32_t* gap = nullptr;
+};
+static std::mutex g_hist_mu;
+static std::map<std::pair<int, int>, HistTablesDev> g_hist_tables;
+
 cudaError_t upload_hist_tables(vox_ctx* c) {
     if (c->d_hist_u) return cudaSuccess;
-    std::vector<float> u;
-    std::vector<uint8_t> perm;
-    std::vector<uint32_t> gap;
-    host_hist_tables(c->hist_n, u, perm, gap);
-    cudaError_t e;
-    if ((e = cudaMalloc((void**)&c->d_hist_u, u.size() * 4)) != cudaSuccess) return e;
-    if ((e = cudaMalloc((void**)&c->d_hist_perm, perm.size())) != cudaSuccess) return e;
-    if ((e = cudaMalloc((void**)&c->d_hist_gap, gap.size() * 4)) != cudaSuccess) return e;
-    // synchronous copies from pageable host vectors (once per ctx)
-    if ((e = cudaMemcpy(c->d_hist_u, u.data(), u.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-    if ((e = cudaMemcpy(c->d_hist_perm, perm.data(), perm.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-    return cudaMemcpy(c->d_hist_gap, gap.data(), gap.size() * 4, cudaMemcpyHostToDevice);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_hist_mu);
+    HistTablesDev& T = g_hist_tables[{dev, c->hist_n}];
+    if (!T.u) {
+        std::vector<float> u;
+        std::vector<uint8_t> perm;
+        std::vector<uint32_t> gap;
+        host_hist_tables(c->hist_n, u, perm, gap);
+        HistTablesDev t;
+        if ((e = cudaMalloc((void**)&t.u, u.size() * 4)) != cudaSuccess) return e;
+        if ((e = cudaMalloc((void**)&t.perm, perm.size())) != cudaSuccess) return e;
+        if ((e = cudaMalloc((void**)&t.gap, gap.size() * 4)) != cudaSuccess) return e;
+        // synchronous copies from pageable host vectors (once per process, device and N)
+        if ((e = cudaMemcpy(t.u, u.data(), u.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+        if ((e = cudaMemcpy(t.perm, perm.data(), perm.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+        if ((e = cudaMemcpy(t.gap, gap.data(), gap.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+        T = t;
+    }
+    c->d_hist_u = T.u;
+    c->d_hist_perm = T.perm;
+    c->d_hist_gap = T.gap;
+    return cudaSuccess;
 }
 
 }  // namespace vox

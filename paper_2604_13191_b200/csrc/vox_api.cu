@@ -677,9 +677,6 @@ void vox_destroy(vox_ctx* c) {
     }
     c->ev_pool.clear();
     if (c->d_lodwork) cudaFreeAsync(c->d_lodwork, c->stream);
-    if (c->d_hist_u) cudaFree(c->d_hist_u);
-    if (c->d_hist_perm) cudaFree(c->d_hist_perm);
-    if (c->d_hist_gap) cudaFree(c->d_hist_gap);
     if (c->d_flags) cudaFreeAsync(c->d_flags, c->stream);
     if (c->d_counter) cudaFreeAsync(c->d_counter, c->stream);
     ssync(c);

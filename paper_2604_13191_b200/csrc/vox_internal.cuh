@@ -160,7 +160,7 @@ struct vox_ctx {
     std::string err;
     int dmode = 0;                          // 0 sigma distance, 1 histogram distance (§10)
     int hist_n = 5000;                      // samples per histogram (§10)
-    float* d_hist_u = nullptr;              // [3][N] sample table (SoA)
+    float* d_hist_u = nullptr;              // [3][N] sample table (SoA); process-wide, not owned
     uint8_t* d_hist_perm = nullptr;         // [124][32] sorted bins per slice (transposed)
     uint32_t* d_hist_gap = nullptr;         // [124][32] fixed-point gaps (transposed)
     // stage timers (profile = 1)
