@@ -75,6 +75,9 @@ def lib():
         L.orc_hist_distance.restype = C.c_int64
         L.orc_hist_distance.argtypes = [u16p, u16p]
         L.orc_sggxh_hist.argtypes = [C.c_int, i64p, C.c_int, C.c_int, i64p]
+        L.orc_jacobi.argtypes = [f32p, f32p]
+        L.orc_encode.argtypes = [C.c_uint64, i64p, u8p, u8p]
+        L.orc_finalize.argtypes = [i64p, f32p]
         _lib = L
     return _lib
 
@@ -267,6 +270,49 @@ def sggxh_hist(acc, k=K_DEFAULT, n=HIST_N_DEFAULT):
     if m < 0:
         raise OracleError(f"sggxh_hist status {m}")
     return out[:m]
+
+
+# ----------------------------------------------------------------- §11 compact form
+
+def jacobi(S6):
+    """Eigenvalues (fp32, unsorted) of the symmetric S given as (xx, yy, zz, xy, xz, yz)."""
+    s, sp = _f32(np.asarray(S6).reshape(6))
+    lam = np.zeros(3, np.float32)
+    lib().orc_jacobi(sp, lam.ctypes.data_as(C.POINTER(C.c_float)))
+    return lam
+
+
+def finalize(acc7):
+    """§11 up to the normalised matrix: (Sn (6,) fp32 as xx, yy, zz, xy, xz, yz, flag) with
+    flag 1 = jittered, 0 = not, -1 = no SGGX (w = 0)."""
+    a, ap = _i64(np.asarray(acc7).reshape(7))
+    Sn = np.zeros(6, np.float32)
+    f = lib().orc_finalize(ap, Sn.ctypes.data_as(C.POINTER(C.c_float)))
+    return Sn, int(f)
+
+
+def encode(acc):
+    """(n,7) int64 (w, M6) records -> ((n,6) uint8 compact SGGX, (n,) uint8 jittered flags)."""
+    a, ap = _i64(np.asarray(acc).reshape(-1, 7))
+    out = np.zeros((a.shape[0], 6), np.uint8)
+    jit = np.zeros(a.shape[0], np.uint8)
+    lib().orc_encode(a.shape[0], ap, out.ctypes.data_as(C.POINTER(C.c_uint8)), jit.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return out, jit
+
+
+def decode(b6):
+    """Renderer-side decode of compact bytes (n,6) -> (n,3,3) fp64 S with negative eigenvalues
+    clamped to 0. Not part of the path; used by the round-trip tests."""
+    b = np.asarray(b6, np.float64).reshape(-1, 6)
+    sg = b[:, :3] / 255.0
+    r = b[:, 3:] / 127.5 - 1.0
+    S = np.zeros((len(b), 3, 3))
+    for a in range(3):
+        S[:, a, a] = sg[:, a] ** 2
+    for (i, j), c in zip(((0, 1), (0, 2), (1, 2)), range(3)):
+        S[:, i, j] = S[:, j, i] = r[:, c] * sg[:, i] * sg[:, j]
+    w, V = np.linalg.eigh(S)
+    return np.einsum("nij,nj,nkj->nik", V, np.maximum(w, 0.0), V)
 
 
 Q = 2.0 ** 32

@@ -913,6 +913,111 @@ int orc_sggxh_hist(int n, const int64_t* acc, int K, int N, int64_t* out) {
     return m;
 }
 
+/* ------------------------------------------------------------------ §11 compact form */
+/* SGGX finalisation: eigenvalues by pinned cyclic Jacobi, degenerate
+ * jitter in moment form, normalisation to max projected area 1, the 6-byte compact
+ * form of Eq. compact-sggx. */
+static void jacobi3(const float S[6], float lam[3]) {
+    float a[3][3] = {{S[0], S[3], S[4]}, {S[3], S[1], S[5]}, {S[4], S[5], S[2]}};
+    static const int PQ[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+    for (int sweep = 0; sweep < 6; sweep++)
+        for (int m = 0; m < 3; m++) {
+            int p = PQ[m][0], q = PQ[m][1], r = 3 - p - q;
+            float apq = a[p][q];
+            if (apq == 0.0f) continue;
+            float th = (a[q][q] - a[p][p]) / (2.0f * apq);
+            float t = 1.0f / (fabsf(th) + sqrtf(th * th + 1.0f));
+            if (th < 0.0f) t = -t;
+            float c = 1.0f / sqrtf(t * t + 1.0f);
+            float sn = t * c;
+            a[p][p] = a[p][p] - t * apq;
+            a[q][q] = a[q][q] + t * apq;
+            a[p][q] = a[q][p] = 0.0f;
+            float arp = a[r][p], arq = a[r][q];
+            a[r][p] = a[p][r] = c * arp - sn * arq;
+            a[r][q] = a[q][r] = sn * arp + c * arq;
+        }
+    lam[0] = a[0][0];
+    lam[1] = a[1][1];
+    lam[2] = a[2][2];
+}
+
+static uint8_t byte_sigma(float x) {
+    int b = (int)floorf(x * 255.0f + 0.5f);
+    return (uint8_t)(b > 255 ? 255 : (b < 0 ? 0 : b));
+}
+static uint8_t byte_r(float r) {
+    int b = (int)floorf((r + 1.0f) * 127.5f + 0.5f);
+    return (uint8_t)(b > 255 ? 255 : (b < 0 ? 0 : b));
+}
+static float corr(float sxy, float sxx, float syy) {
+    float p = sxx * syy;
+    float r = p > 0.0f ? sxy / sqrtf(p) : 0.0f;
+    return r > 1.0f ? 1.0f : (r < -1.0f ? -1.0f : r);
+}
+
+/* §11 up to the normalised matrix: Sn [6]; returns 1 iff jittered, -1 if there is no SGGX
+ * (w = 0 or max eigenvalue <= 0; Sn zero) */
+static int finalize6(const i128 acc[7], float Sn[6]) {
+    for (int e = 0; e < 6; e++) Sn[e] = 0.0f;
+    if (acc[0] == 0) return -1;
+    float wf = deq32(acc[0]);
+    float S[6];
+    for (int e = 0; e < 6; e++) S[e] = deq32(acc[1 + e]) / wf;
+    float tr = (S[0] + S[1]) + S[2];
+    float lam[3];
+    jacobi3(S, lam);
+    float lmax = lam[0], lmin = lam[0];
+    for (int a = 1; a < 3; a++) {
+        if (lam[a] > lmax) lmax = lam[a];
+        if (lam[a] < lmin) lmin = lam[a];
+    }
+    int jit = lmin < 1e-4f * lmax;
+    if (jit) {
+        const float C1 = 0.9999f, C2 = (float)(1e-4 / 3.0);
+        for (int e = 0; e < 6; e++) S[e] = e < 3 ? C1 * S[e] + C2 * tr : C1 * S[e];
+        lmax = C1 * lmax + C2 * tr;
+    }
+    if (!(lmax > 0.0f)) return -1;
+    float inv = 1.0f / lmax;
+    for (int e = 0; e < 6; e++) Sn[e] = S[e] * inv;
+    return jit;
+}
+
+/* returns 1 iff the record was jittered */
+static int encode6(const i128 acc[7], uint8_t out[6]) {
+    static const uint8_t ZERO[6] = {0, 0, 0, 128, 128, 128};
+    memcpy(out, ZERO, 6);
+    float Sn[6];
+    int jit = finalize6(acc, Sn);
+    if (jit < 0) return 0;
+    out[0] = byte_sigma(sqrtf(fmaxf_(Sn[0], 0.0f)));
+    out[1] = byte_sigma(sqrtf(fmaxf_(Sn[1], 0.0f)));
+    out[2] = byte_sigma(sqrtf(fmaxf_(Sn[2], 0.0f)));
+    out[3] = byte_r(corr(Sn[3], Sn[0], Sn[1]));
+    out[4] = byte_r(corr(Sn[4], Sn[0], Sn[2]));
+    out[5] = byte_r(corr(Sn[5], Sn[1], Sn[2]));
+    return jit;
+}
+
+int orc_finalize(const int64_t acc7[7], float Sn[6]) {
+    i128 a[7];
+    for (int e = 0; e < 7; e++) a[e] = acc7[e];
+    return finalize6(a, Sn);
+}
+
+void orc_jacobi(const float S[6], float lam[3]) { jacobi3(S, lam); }
+
+/* n records of int64 (w, M6) -> out [n][6]; jit [n] (nullable) */
+void orc_encode(uint64_t n, const int64_t* acc, uint8_t* out, uint8_t* jit) {
+    for (uint64_t x = 0; x < n; x++) {
+        i128 a[7];
+        for (int e = 0; e < 7; e++) a[e] = acc[7 * x + e];
+        int j = encode6(a, out + 6 * x);
+        if (jit) jit[x] = (uint8_t)j;
+    }
+}
+
 static int cmp_rec(const void* x, const void* y) {
     uint64_t a = ((const rec_t*)x)->key, b = ((const rec_t*)y)->key;
     return a < b ? -1 : a > b;
