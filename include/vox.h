@@ -86,6 +86,7 @@ typedef struct {
      * (32 slices each), pair distance evaluations (32 slices each), parents with n > k */
     uint64_t lod_sigma_evals, lod_dist_evals, lod_hard_parents;
     double host_ms_alloc, host_ms_sync;   /* host time in stream-ordered allocation / stream syncs */
+    double ms_encode;      /* vox_encode_level device time (profile=1) */
 } vox_stats;
 
 /* Create a ctx for an N^3 grid over the cubic extent of bbox (D3).
@@ -131,6 +132,19 @@ vox_status vox_read_level(vox_ctx* ctx, uint32_t level, vox_level_view* out);
  * and cl = (mass, M) in slot 0. Synchronises the ctx stream when a buffer is host memory. */
 vox_status vox_copy_level(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                           uint8_t* ncl, float* cl);
+
+/* SGGX finalisation and the 6-byte compact form (PREDICATES §11; Eq. compact-sggx P:354-362,
+ * SPEC S:47) of every record of a level, into
+ * caller-owned DEVICE buffers (stream-ordered on the ctx stream, no sync):
+ *   sggx6 [n][6]    the voxel's aggregate (mass, M): sigma_x, sigma_y, sigma_z bytes
+ *                   (round(sigma*255)), r_xy, r_xz, r_yz bytes (round((r+1)*127.5)), after
+ *                   the degenerate jitter (lambda_min < 1e-4 lambda_max) and normalisation to
+ *                   maximum projected area 1; a record with w = 0 is (0,0,0,128,128,128);
+ *   cl6   [n][k][6] the voxel's SGGX-H lobes, slots >= ncl as for w = 0 (NULL: skipped);
+ *                   at level 0 slot 0 is the voxel itself;
+ *   flags [n]       bit 0: aggregate jittered, bit 1+q: lobe q jittered (NULL: skipped).
+ * level > built -> VOX_ERR_LEVEL; sggx6 NULL -> VOX_ERR_INVALID_ARG. */
+vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags);
 
 /* Copy a level's exact accumulators acc [n][7] (int64, quantum 2^-32; device or host). */
 vox_status vox_copy_level_acc(vox_ctx* ctx, uint32_t level, int64_t* acc);

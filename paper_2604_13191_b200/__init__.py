@@ -52,7 +52,8 @@ class _Stats(C.Structure):
                 ("ms_lod_prep", C.c_double), ("ms_sggxh_quad", C.c_double),
                 ("ms_sggxh_half", C.c_double), ("ms_sggxh_warp", C.c_double),
                 ("launches", C.c_uint64), ("lod_sigma_evals", C.c_uint64), ("lod_dist_evals", C.c_uint64),
-                ("lod_hard_parents", C.c_uint64), ("host_ms_alloc", C.c_double), ("host_ms_sync", C.c_double)]
+                ("lod_hard_parents", C.c_uint64), ("host_ms_alloc", C.c_double), ("host_ms_sync", C.c_double),
+                ("ms_encode", C.c_double)]
 
 
 _lib = None
@@ -77,6 +78,7 @@ def lib():
     L.vox_read_level.argtypes = [vp, u32, C.POINTER(_View)]
     L.vox_copy_level.argtypes = [vp, u32, vp, vp, vp, vp, vp]
     L.vox_copy_level_acc.argtypes = [vp, u32, vp]
+    L.vox_encode_level.argtypes = [vp, u32, vp, vp, vp]
     L.vox_export_level.argtypes = [vp, u32, vp, C.POINTER(u64)]
     L.vox_import_level.argtypes = [vp, u32, vp, u64]
     L.vox_plan_shards.argtypes = [C.POINTER(u64), u64, i32, C.POINTER(u64)]
@@ -93,7 +95,7 @@ def lib():
     L.vox_destroy.argtypes = [vp]
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
-                 "vox_copy_level", "vox_copy_level_acc", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
+                 "vox_copy_level", "vox_copy_level_acc", "vox_encode_level", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
     _lib = L
@@ -279,6 +281,22 @@ class Vox:
         ptr = lambda k: out[k].data_ptr() if k in out and out[k] is not None else None
         self._check(lib().vox_copy_level(self._h, int(level), ptr("key"), ptr("mass"), ptr("m6"), ptr("ncl"),
                                          ptr("cl")), "copy_level")
+
+    def encode_level(self, level: int, lobes: bool = True, flags: bool = True) -> dict:
+        """vox_encode_level (PREDICATES §11): the 6-byte compact SGGX of every voxel
+        (sggx6 uint8 [n,6]) and, optionally, of its lobes (cl6 uint8 [n,k,6]) and the jitter
+        flags (uint8 [n]) as cuda tensors."""
+        import torch
+        n = int(self.view(level)["n"])
+        out = {"sggx6": torch.empty((max(n, 1), 6), dtype=torch.uint8, device="cuda")}
+        if lobes:
+            out["cl6"] = torch.empty((max(n, 1), self.k, 6), dtype=torch.uint8, device="cuda")
+        if flags:
+            out["flags"] = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+        ptr = lambda k: out[k].data_ptr() if k in out else None
+        self._check(lib().vox_encode_level(self._h, int(level), ptr("sggx6"), ptr("cl6"), ptr("flags")),
+                    "encode_level")
+        return {k: t[:n] for k, t in out.items()}
 
     # ------------------------------------------------------------------ multi-GPU records
     def export_level(self, level: int):

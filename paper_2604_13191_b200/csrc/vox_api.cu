@@ -516,6 +516,16 @@ __global__ void k_leaf_lobes(uint64_t n, const float* __restrict__ mass, const f
     }
 }
 
+vox_status vox_encode_level(vox_ctx* c, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags) {
+    if (!c || !sggx6) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    timer_begin(c, c->t_encode);
+    CKS(launch_encode(c, c->lv[level], level == 0, sggx6, cl6, flags));
+    timer_end(c, c->t_encode);
+    c->st.launches++;
+    return VOX_OK;
+}
+
 vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass, float* m6, uint8_t* ncl, float* cl) {
     if (!c) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
@@ -623,6 +633,7 @@ vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     c->st.ms_sggxh_quad = timer_flush(c, c->t_quad);
     c->st.ms_sggxh_half = timer_flush(c, c->t_half);
     c->st.ms_sggxh_warp = timer_flush(c, c->t_warp);
+    c->st.ms_encode = timer_flush(c, c->t_encode);
     if (c->d_lodwork) {
         unsigned long long w[3] = {0, 0, 0};
         CKS(cudaMemcpy(w, c->d_lodwork, 24, cudaMemcpyDeviceToHost));
@@ -639,7 +650,7 @@ vox_status vox_stats_reset(vox_ctx* c) {
     vox_stats tmp;
     vox_stats_get(c, &tmp);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp})
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode})
         t->ms = 0.0;
     c->st.launches = 0;
     c->st.host_ms_alloc = c->st.host_ms_sync = 0;
@@ -667,7 +678,7 @@ void vox_destroy(vox_ctx* c) {
     ssync(c);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp}) {
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode}) {
         timer_flush(c, *t);
         if (t->open) cudaEventDestroy(t->open);
     }

@@ -164,7 +164,7 @@ struct vox_ctx {
     uint8_t* d_hist_perm = nullptr;         // [124][32] sorted bins per slice (transposed)
     uint32_t* d_hist_gap = nullptr;         // [124][32] fixed-point gaps (transposed)
     // stage timers (profile = 1)
-    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp;
+    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp, t_encode;
 };
 
 namespace vox {
@@ -203,6 +203,8 @@ void upload_theta(vox_ctx* c);
 // histogram distance (k_hist.cu)
 void host_hist_tables(int N, std::vector<float>& u, std::vector<uint8_t>& permT, std::vector<uint32_t>& gapT);
 cudaError_t upload_hist_tables(vox_ctx* c);
+// compact form (k_encode.cu)
+cudaError_t launch_encode(vox_ctx* c, const Level& L, int leaf, uint8_t* out6, uint8_t* cl6, uint8_t* flags);
 cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
                               int leaf, const uint32_t* start, Level& P);
 void host_theta(float theta[32][3], float coef[32][6]);

@@ -8,6 +8,7 @@ import torch
 
 import gen
 import oracle
+from windowing import window_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -20,33 +21,10 @@ def _cells(keys0, level, count, rng):
     return [int(c) for c in pick]
 
 
-def _window_oracle(c, level, cell):
-    N, bbox = c["grid_res"], c["bbox"]
-    E = float(np.max(bbox[3:] - bbox[:3]))
-    i, j, k = oracle.unmorton(cell)
-    lo_box = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
-    hi_box = lo_box + ((1 << level) + 4) * E / N
-    o = oracle.Oracle(N, bbox)
-    o.set_window(level, cell)
-    if c["kind"] == "fiber":
-        s, r = c["segments"], c["radii"]
-        lo = np.minimum(s[:, 0], s[:, 1]) - r[:, None]
-        hi = np.maximum(s[:, 0], s[:, 1]) + r[:, None]
-        sel = np.all((hi >= lo_box) & (lo <= hi_box), axis=1)
-        o.add_fibers(np.ascontiguousarray(s[sel]), np.ascontiguousarray(r[sel]))
-    else:
-        t = c["tris"]
-        sel = np.all((t.max(1) >= lo_box) & (t.min(1) <= hi_box), axis=1)
-        d = None if c["dirs"] is None else np.ascontiguousarray(c["dirs"][sel])
-        o.add_triangles(np.ascontiguousarray(t[sel]), d)
-    o.build(level)
-    return o
-
-
 def _check(v, c, level, cells):
     levels = [v.level(l) for l in range(level + 1)]      # device copies; cells selected on the GPU
     for cell in cells:
-        o = _window_oracle(c, level, cell)
+        o = window_oracle(c, level, cell)
         for l in range(level + 1):
             g = levels[l]
             sel = (g["key"] >> (3 * (level - l))) == cell
