@@ -176,6 +176,7 @@ def main():
     ap.add_argument("--hist-samples", type=int, default=5000, help="N samples per SGGX histogram (P:389)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-finalize", action="store_true", help="skip the compact-form (NEXT-3) measurement")
     ap.add_argument("--cpu-segments", type=int, default=400_000, help="oracle sample size (cpu_baseline)")
     ap.add_argument("--ref-segments", type=int, default=40_000, help="oracle sample size per reference step")
     args = ap.parse_args()
@@ -376,6 +377,25 @@ def main():
                        "d2h_bytes_per_step": int(outs["d2h"]),
                        "wall_s": time.perf_counter() - t0}
     line["clocks"] = clk.summary()
+
+    # ---------------------------------------------------------------- NEXT-3: compact form of every level
+    # (not part of the timed step: one extra build, then vox_encode_level on levels 0..L, device time
+    # from the library's events)
+    if not args.no_finalize:
+        v = step(profile=True)
+        v.stats_reset()
+        bufs = []
+        for l in range(levels + 1):
+            bufs.append(v.encode_level(l))
+        st = v.stats()
+        recs = V[0] + sum(V[l] * (1 + v.k) for l in range(1, levels + 1))
+        byts = V[0] * (56 + 6 + 6 * v.k + 1) + sum(V[l] * (56 + 1 + 56 * v.k + 6 + 6 * v.k + 1)
+                                                    for l in range(1, levels + 1))
+        line["finalize"] = {"ms": st["ms_encode"], "records": recs, "records_per_s": recs / (st["ms_encode"] / 1e3),
+                            "alg_bytes": byts, "achieved_gbs": byts / (st["ms_encode"] / 1e3) / 1e9,
+                            "bound": "alu (pinned Jacobi: ~18 rotations with IEEE div/sqrt per record)"}
+        v.close()
+        del bufs
 
     # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
     if rank == 0 and world == 1 and not args.no_cpu_baseline and fib:
