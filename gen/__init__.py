@@ -232,3 +232,20 @@ def config(n: int, **kw) -> dict:
         s, r, bb = knit(S, seed=5, grid_res=N, seg_len_vox=3.0 * N / 4096, radius_vox=0.5 * N / 4096)
         return dict(kind="fiber", grid_res=N, levels=int(math.log2(N)), bbox=bb, segments=s, radii=r)
     raise ValueError(n)
+
+
+def splines_from_segments(seg):
+    """Catmull-Rom controls [S,4,3] for consecutive fiber segments [S,2,3] (input preparation
+    for the sampling front end, PREDICATES §12): piece i runs seg[i,0] -> seg[i,1]; its outer
+    controls are the neighbouring nodes of the same fiber (segments chained end to start), or
+    the end node reflected (2 P1 - P2, 2 P2 - P1) at a fiber end."""
+    seg = np.asarray(seg, np.float32)
+    P1, P2 = seg[:, 0], seg[:, 1]
+    prev_ok = np.zeros(len(seg), bool)
+    prev_ok[1:] = np.all(seg[:-1, 1] == seg[1:, 0], axis=1)
+    next_ok = np.zeros(len(seg), bool)
+    next_ok[:-1] = prev_ok[1:]
+    P0 = np.where(prev_ok[:, None], np.roll(P1, 1, axis=0), 2 * P1 - P2)
+    P3 = np.where(next_ok[:, None], np.roll(P2, -1, axis=0), 2 * P2 - P1)
+    return np.ascontiguousarray(np.stack([P0, P1, P2, P3], 1).astype(np.float32))
+

@@ -78,6 +78,11 @@ def lib():
         L.orc_jacobi.argtypes = [f32p, f32p]
         L.orc_encode.argtypes = [C.c_uint64, i64p, u8p, u8p]
         L.orc_finalize.argtypes = [i64p, f32p]
+        L.orc_spline_eval.argtypes = [f32p, C.c_float, f32p, f32p]
+        L.orc_sample_splines.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64, C.c_int]
+        L.orc_sample_triangles.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64, C.c_int]
+        L.orc_tri_samples.argtypes = [C.c_float, C.c_float, C.c_int]
+        L.orc_tri_sample_points.argtypes = [f32p, C.c_int, f32p]
         _lib = L
     return _lib
 
@@ -141,6 +146,21 @@ class Oracle:
             d, dp = _f32(np.asarray(dirs).reshape(-1, 3))
             assert d.shape[0] == t.shape[0]
         _check(lib().orc_add_triangles(self._h, tp, dp, t.shape[0]), "add_triangles")
+
+    def sample_splines(self, ctrl, radii, n: int):
+        """§12: Catmull-Rom pieces (controls [S,4,3] world, radii [S]), n samples per piece."""
+        cc, cp = _f32(np.asarray(ctrl).reshape(-1, 12))
+        r, rp = _f32(np.asarray(radii).reshape(-1))
+        assert cc.shape[0] == r.shape[0]
+        _check(lib().orc_sample_splines(self._h, cp, rp, cc.shape[0], int(n)), "sample_splines")
+
+    def sample_triangles(self, tris, dirs=None, budget: int = 64):
+        """§12: triangles sampled with Heitz's map, budget samples for the largest one."""
+        t, tp = _f32(np.asarray(tris).reshape(-1, 9))
+        dp = None
+        if dirs is not None:
+            d, dp = _f32(np.asarray(dirs).reshape(-1, 3))
+        _check(lib().orc_sample_triangles(self._h, tp, dp, t.shape[0], int(budget)), "sample_triangles")
 
     def build(self, levels: int = 0):
         _check(lib().orc_build(self._h, int(levels)), "build")
@@ -270,6 +290,29 @@ def sggxh_hist(acc, k=K_DEFAULT, n=HIST_N_DEFAULT):
     if m < 0:
         raise OracleError(f"sggxh_hist status {m}")
     return out[:m]
+
+
+# ----------------------------------------------------------------- §12 sampling front end
+
+def spline_eval(G, t):
+    """Grid-space Catmull-Rom piece G [4,3] at t -> (position (3,), unit tangent (3,))."""
+    g, gp = _f32(np.asarray(G).reshape(12))
+    pos = np.zeros(3, np.float32)
+    tan = np.zeros(3, np.float32)
+    lib().orc_spline_eval(gp, C.c_float(t), pos.ctypes.data_as(C.POINTER(C.c_float)),
+                          tan.ctypes.data_as(C.POINTER(C.c_float)))
+    return pos, tan
+
+
+def tri_samples(area, amax, budget) -> int:
+    return int(lib().orc_tri_samples(C.c_float(area), C.c_float(amax), int(budget)))
+
+
+def tri_sample_points(g9, n):
+    g, gp = _f32(np.asarray(g9).reshape(9))
+    out = np.zeros((n, 3), np.float32)
+    lib().orc_tri_sample_points(gp, int(n), out.ctypes.data_as(C.POINTER(C.c_float)))
+    return out
 
 
 # ----------------------------------------------------------------- §11 compact form

@@ -625,6 +625,170 @@ int orc_add_triangles(orc_ctx* c, const float* tri, const float* dirs, uint64_t 
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------ §12 sampling front end */
+/* The paper's own voxelization: Catmull-Rom spline pieces sampled at
+ * t_s = (s + 1/2)/n and triangles sampled with Heitz's low-distortion map,
+ * sample counts proportional to area; each sample adds to the voxel containing it. */
+static int push_sample(orc_ctx* c, const float p[3], float f, const float d[3]) {
+    int64_t v[3];
+    for (int ax = 0; ax < 3; ax++) {
+        float fl_ = floorf(p[ax]);
+        if (!(fl_ >= 0.0f) || !(fl_ < (float)c->g.N)) return ORC_OK; /* outside [0, N): dropped */
+        v[ax] = (int64_t)fl_;
+    }
+    if (!in_window(c, v[0], v[1], v[2])) return ORC_OK;
+    int64_t q[7];
+    q[0] = q32(f);
+    q[1] = q32((f * d[0]) * d[0]);
+    q[2] = q32((f * d[1]) * d[1]);
+    q[3] = q32((f * d[2]) * d[2]);
+    q[4] = q32((f * d[0]) * d[1]);
+    q[5] = q32((f * d[0]) * d[2]);
+    q[6] = q32((f * d[1]) * d[2]);
+    return push_rec(c, orc_morton((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2]), q);
+}
+
+/* position and unit tangent of a grid-space Catmull-Rom piece at t (§12) */
+static void spline_eval(const float G[4][3], float t, float pos[3], float tan_[3]) {
+    float dv[3];
+    for (int ax = 0; ax < 3; ax++) {
+        float c0 = 2.0f * G[1][ax];
+        float c1 = G[2][ax] - G[0][ax];
+        float c2 = ((2.0f * G[0][ax] - 5.0f * G[1][ax]) + 4.0f * G[2][ax]) - G[3][ax];
+        float c3 = ((3.0f * G[1][ax] - G[0][ax]) - 3.0f * G[2][ax]) + G[3][ax];
+        pos[ax] = 0.5f * (((c3 * t + c2) * t + c1) * t + c0);
+        dv[ax] = 0.5f * ((3.0f * c3 * t + 2.0f * c2) * t + c1);
+    }
+    float nn = dv[0] * dv[0] + dv[1] * dv[1];
+    nn = nn + dv[2] * dv[2];
+    float nrm = sqrtf(nn);
+    for (int ax = 0; ax < 3; ax++) tan_[ax] = nrm > 0.0f ? dv[ax] / nrm : 0.0f;
+}
+
+void orc_spline_eval(const float G[12], float t, float pos[3], float tan_[3]) {
+    spline_eval((const float(*)[3])G, t, pos, tan_);
+}
+
+int orc_sample_splines(orc_ctx* c, const float* ctrl, const float* radii, uint64_t S, int n) {
+    const float PI_F = 3.14159274101257324f;
+    if (n < 1) return ORC_ERR_ARG;
+    c->built = -1;
+    for (uint64_t p = 0; p < S; p++) {
+        float G[4][3];
+        for (int m = 0; m < 4; m++)
+            for (int ax = 0; ax < 3; ax++) {
+                float w = ctrl[12 * p + 3 * m + ax];
+                if (!isfinite(w)) return ORC_ERR_ARG;
+                G[m][ax] = grid_coord(&c->g, ax, w);
+            }
+        float r = radii[p];
+        if (!isfinite(r) || r < 0.0f) return ORC_ERR_ARG;
+        float rg = grid_len(&c->g, r);
+        float d[3] = {G[2][0] - G[1][0], G[2][1] - G[1][1], G[2][2] - G[1][2]};
+        float dd = d[0] * d[0] + d[1] * d[1];
+        dd = dd + d[2] * d[2];
+        float mp = PI_F * rg;
+        mp = mp * rg;
+        mp = mp * sqrtf(dd);
+        float f = mp / (float)n;
+        for (int s = 0; s < n; s++) {
+            float t = ((float)s + 0.5f) / (float)n;
+            float pos[3], tan_[3];
+            spline_eval((const float(*)[3])G, t, pos, tan_);
+            int rc = push_sample(c, pos, f, tan_);
+            if (rc) return rc;
+        }
+    }
+    return ORC_OK;
+}
+
+/* whole-triangle area (§7 area formula, one fan term) and direction (§7) in grid space */
+static float tri_whole_area(const float g[9]) {
+    float e1[3], e2[3], cr[3];
+    for (int ax = 0; ax < 3; ax++) { e1[ax] = g[3 + ax] - g[ax]; e2[ax] = g[6 + ax] - g[ax]; }
+    cross3(e1, e2, cr);
+    float acc[3] = {0.0f + cr[0], 0.0f + cr[1], 0.0f + cr[2]};
+    float nn = acc[0] * acc[0] + acc[1] * acc[1];
+    nn = nn + acc[2] * acc[2];
+    return 0.5f * sqrtf(nn);
+}
+
+int orc_tri_samples(float A, float Amax, int budget) {
+    if (!(A > 0.0f)) return 0;
+    int k = (int)floorf((A / Amax) * (float)budget + 0.5f);
+    return k < 1 ? 1 : k;
+}
+
+void orc_tri_uv(int s, int n, float* u0, float* u1) {
+    *u0 = ((float)s + 0.5f) / (float)n;
+    float x = (float)s * 0.618034f;
+    *u1 = x - floorf(x);
+}
+
+/* unit entry for tests: the n sample points (grid space) of one grid-space triangle */
+void orc_tri_sample_points(const float g[9], int n, float* out) {
+    for (int s = 0; s < n; s++) {
+        float u0, u1, b0, b1;
+        orc_tri_uv(s, n, &u0, &u1);
+        if (u1 > u0) { b0 = 0.5f * u0; b1 = u1 - b0; }
+        else { b1 = 0.5f * u1; b0 = u0 - b1; }
+        float b2 = (1.0f - b0) - b1;
+        for (int ax = 0; ax < 3; ax++) out[3 * s + ax] = (b0 * g[ax] + b1 * g[3 + ax]) + b2 * g[6 + ax];
+    }
+}
+
+int orc_sample_triangles(orc_ctx* c, const float* tri, const float* dirs, uint64_t T, int budget) {
+    if (budget < 1) return ORC_ERR_ARG;
+    c->built = -1;
+    float Amax = 0.0f;
+    for (uint64_t t = 0; t < T; t++) {
+        float g[9];
+        for (int q = 0; q < 9; q++) {
+            if (!isfinite(tri[9 * t + q])) return ORC_ERR_ARG;
+            g[q] = grid_coord(&c->g, q % 3, tri[9 * t + q]);
+        }
+        float A = tri_whole_area(g);
+        if (A > Amax) Amax = A;
+    }
+    for (uint64_t t = 0; t < T; t++) {
+        float g[9];
+        for (int q = 0; q < 9; q++) g[q] = grid_coord(&c->g, q % 3, tri[9 * t + q]);
+        float w[3];
+        if (dirs) {
+            for (int ax = 0; ax < 3; ax++) {
+                w[ax] = dirs[3 * t + ax];
+                if (!isfinite(w[ax])) return ORC_ERR_ARG;
+            }
+        } else {
+            float f1[3], f2[3];
+            for (int ax = 0; ax < 3; ax++) { f1[ax] = g[3 + ax] - g[ax]; f2[ax] = g[6 + ax] - g[3 + ax]; }
+            cross3(f1, f2, w);
+        }
+        float nn = w[0] * w[0] + w[1] * w[1];
+        nn = nn + w[2] * w[2];
+        float nrm = sqrtf(nn);
+        if (dirs && !(nrm > 0.0f)) return ORC_ERR_ARG;
+        float dh[3];
+        for (int ax = 0; ax < 3; ax++) dh[ax] = nrm > 0.0f ? w[ax] / nrm : 0.0f;
+        float A = tri_whole_area(g);
+        int nt = orc_tri_samples(A, Amax, budget);
+        if (nt == 0) continue;
+        float f = A / (float)nt;
+        for (int s = 0; s < nt; s++) {
+            float u0, u1, b0, b1;
+            orc_tri_uv(s, nt, &u0, &u1);
+            if (u1 > u0) { b0 = 0.5f * u0; b1 = u1 - b0; }
+            else { b1 = 0.5f * u1; b0 = u0 - b1; }
+            float b2 = (1.0f - b0) - b1;
+            float p[3];
+            for (int ax = 0; ax < 3; ax++) p[ax] = (b0 * g[ax] + b1 * g[3 + ax]) + b2 * g[6 + ax];
+            int rc = push_sample(c, p, f, dh);
+            if (rc) return rc;
+        }
+    }
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------ §9 SGGX-H */
 
 static void theta_table(float theta[32][3], float coef[32][6]) {
