@@ -133,6 +133,22 @@ vox_status vox_read_level(vox_ctx* ctx, uint32_t level, vox_level_view* out);
 vox_status vox_copy_level(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                           uint8_t* ncl, float* cl);
 
+/* The paper's own sampling front end (PREDICATES §12; §3.2):
+ * primitives become samples, each sample adds (mass, mass * d d^T) to the voxel containing it
+ * (half-open cells, samples outside [0,N)^3 dropped); the pairs go through the same binned
+ * reduce as the exact path and calls accumulate with every other voxelize call (D19).
+ *   vox_sample_splines: Catmull-Rom pieces, ctrl dev f32 [S][4][3] (P0..P3 world; the piece
+ *     runs P1 -> P2), radii dev f32 [S]; n samples per piece at t = (s + 1/2)/n, each
+ *     with mass pi r^2 |P2 - P1| / n (grid units) and the curve's unit tangent.
+ *     n in 1..65536 and S * n < 2^32, else VOX_ERR_INVALID_ARG.
+ *   vox_sample_triangles: tris dev f32 [T][3][3], dirs dev f32 [T][3] or NULL (face normals);
+ *     round(budget * A / A_max) samples per triangle (>= 1 if A > 0; A_max over the call,
+ *     P:228) placed by Heitz's low-distortion square -> triangle map, each with mass
+ *     A / n_t. budget in 1..65536.
+ * Non-finite input, negative radius or zero dirs -> VOX_ERR_INVALID_ARG at the call's sync. */
+vox_status vox_sample_splines(vox_ctx* ctx, const float* ctrl, const float* radii, uint64_t S, uint32_t n);
+vox_status vox_sample_triangles(vox_ctx* ctx, const float* tris, const float* dirs, uint64_t T, uint32_t budget);
+
 /* SGGX finalisation and the 6-byte compact form (PREDICATES §11; Eq. compact-sggx P:354-362,
  * SPEC S:47) of every record of a level, into
  * caller-owned DEVICE buffers (stream-ordered on the ctx stream, no sync):

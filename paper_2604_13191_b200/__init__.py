@@ -79,6 +79,8 @@ def lib():
     L.vox_copy_level.argtypes = [vp, u32, vp, vp, vp, vp, vp]
     L.vox_copy_level_acc.argtypes = [vp, u32, vp]
     L.vox_encode_level.argtypes = [vp, u32, vp, vp, vp]
+    L.vox_sample_splines.argtypes = [vp, vp, vp, u64, u32]
+    L.vox_sample_triangles.argtypes = [vp, vp, vp, u64, u32]
     L.vox_export_level.argtypes = [vp, u32, vp, C.POINTER(u64)]
     L.vox_import_level.argtypes = [vp, u32, vp, u64]
     L.vox_plan_shards.argtypes = [C.POINTER(u64), u64, i32, C.POINTER(u64)]
@@ -95,7 +97,8 @@ def lib():
     L.vox_destroy.argtypes = [vp]
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
-                 "vox_copy_level", "vox_copy_level_acc", "vox_encode_level", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
+                 "vox_copy_level", "vox_copy_level_acc", "vox_encode_level", "vox_sample_splines",
+                 "vox_sample_triangles", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
     _lib = L
@@ -281,6 +284,24 @@ class Vox:
         ptr = lambda k: out[k].data_ptr() if k in out and out[k] is not None else None
         self._check(lib().vox_copy_level(self._h, int(level), ptr("key"), ptr("mass"), ptr("m6"), ptr("ncl"),
                                          ptr("cl")), "copy_level")
+
+    def sample_splines(self, ctrl, radii, n: int):
+        """vox_sample_splines (PREDICATES §12): Catmull-Rom pieces ctrl [S,4,3] and radii [S]
+        (cuda float32), n samples per piece."""
+        c = _dev_f32(ctrl, "ctrl", (4, 3))
+        r = _dev_f32(radii, "radii", ())
+        if r.shape[0] != c.shape[0]:
+            raise ValueError("ctrl and radii disagree on S")
+        self._check(lib().vox_sample_splines(self._h, c.data_ptr(), r.data_ptr(), c.shape[0], int(n)),
+                    "sample_splines")
+
+    def sample_triangles(self, tris, dirs=None, budget: int = 64):
+        """vox_sample_triangles (PREDICATES §12): tris [T,3,3] (+ dirs [T,3]) cuda float32,
+        `budget` samples for the largest triangle."""
+        t = _dev_f32(tris, "tris", (3, 3))
+        d = None if dirs is None else _dev_f32(dirs, "dirs", (3,))
+        self._check(lib().vox_sample_triangles(self._h, t.data_ptr(), None if d is None else d.data_ptr(),
+                                               t.shape[0], int(budget)), "sample_triangles")
 
     def encode_level(self, level: int, lobes: bool = True, flags: bool = True) -> dict:
         """vox_encode_level (PREDICATES §11): the 6-byte compact SGGX of every voxel

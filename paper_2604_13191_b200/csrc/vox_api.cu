@@ -285,7 +285,8 @@ static int bin_log2(const vox_ctx* c) { return std::min(c->g.logN >= 13 ? 5 : 4,
 static uint64_t nbins_of(const vox_ctx* c) { return 1ull << (3 * (c->g.logN - bin_log2(c))); }
 
 static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* Wb,
-                                  emit_fn emit) {
+                                  emit_fn emit, uint64_t nptab = 0) {
+    if (nptab == 0) nptab = n;   // prim-table entries (one per sample for the spline front end)
     const uint64_t ncells = ncells_of(c), nb = nbins_of(c);
     const int Lb = bin_log2(c);
     unsigned fl = 0;
@@ -336,7 +337,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
         return VOX_OK;
     }
     // estimate: pairs + per-bin scans + new leaf (<= cap voxels) + prim table + merge
-    const uint64_t est = cap * 16 + nb * 24 + cap * 92 + n * 16 + c->lv[0].n * 92;
+    const uint64_t est = cap * 16 + nb * 24 + cap * 92 + nptab * 16 + c->lv[0].n * 92;
     if (c->max_bytes && est > c->max_bytes) {
         dfree(c, off);
         c->err = "estimated " + std::to_string(est) + " bytes exceed max_bytes";
@@ -347,7 +348,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     unsigned* bcnt = nullptr;
     CKS(dalloc(c, (void**)&keys, cap * 8));
     CKS(dalloc(c, (void**)&vals, cap * 8));
-    CKS(dalloc(c, (void**)&ptab, n * sizeof(float4)));
+    CKS(dalloc(c, (void**)&ptab, nptab * sizeof(float4)));
     CKS(dalloc(c, (void**)&bcnt, nb * 4));
     CKS(cudaMemsetAsync(bcnt, 0, nb * 4, c->stream));
     Shard sh;
@@ -426,6 +427,66 @@ vox_status vox_voxelize_triangles(vox_ctx* c, const float* tris, const float* di
     CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
     CKS(launch_tri_bound(c, tris, dirs, T, cellW, bin_log2(c)));
     s = voxelize_common(c, tris, dirs, T, cellW, emit_tris);
+    timer_end(c, c->t_vox);
+    return s;
+}
+
+// ---------------------------------------------------------------- the paper's sampling front end (§12)
+static cudaError_t emit_splines(vox_ctx* c, const float* ctrl, const float* rad, uint64_t S, Shard sh, Bins bins,
+                                uint64_t* keys, uint64_t* vals, float4* ptab) {
+    return launch_spline_emit(c, ctrl, rad, S, c->samp_n, sh, bins, keys, vals, ptab);
+}
+
+static cudaError_t emit_sampled_tris(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh,
+                                     Bins bins, uint64_t* keys, uint64_t* vals, float4* ptab) {
+    return launch_tris_emit(c, tri, dirs, T, c->samp_n, c->samp_amax, sh, bins, keys, vals, ptab);
+}
+
+vox_status vox_sample_splines(vox_ctx* c, const float* ctrl, const float* radii, uint64_t S, uint32_t n) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (S == 0) return VOX_OK;
+    if (!ctrl || !radii || n < 1 || n > 65536 || S * (uint64_t)n >= (1ull << 32)) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    c->st.segments = S;
+    timer_begin(c, c->t_vox);
+    timer_begin(c, c->t_bound);
+    const uint64_t nb = nbins_of(c);
+    unsigned long long* cellW = nullptr;
+    CKS(dalloc(c, (void**)&cellW, nb * 8));
+    CKS(cudaMemsetAsync(cellW, 0, nb * 8, c->stream));
+    CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
+    CKS(launch_spline_bound(c, ctrl, radii, S, (int)n, cellW, bin_log2(c)));
+    c->samp_n = (int)n;
+    s = voxelize_common(c, ctrl, radii, S, cellW, emit_splines, S * (uint64_t)n);
+    timer_end(c, c->t_vox);
+    return s;
+}
+
+vox_status vox_sample_triangles(vox_ctx* c, const float* tris, const float* dirs, uint64_t T, uint32_t budget) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->state == ST_LOD) return VOX_ERR_STATE;
+    if (T == 0) return VOX_OK;
+    if (!tris || budget < 1 || budget > 65536 || T >= (1ull << 32)) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    c->st.segments = T;
+    timer_begin(c, c->t_vox);
+    timer_begin(c, c->t_bound);
+    const uint64_t nb = nbins_of(c);
+    unsigned long long* cellW = nullptr;
+    CKS(dalloc(c, (void**)&cellW, nb * 8));
+    CKS(cudaMemsetAsync(cellW, 0, nb * 8, c->stream));
+    CKS(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
+    unsigned* amax = nullptr;
+    CKS(dalloc(c, (void**)&amax, 16));
+    CKS(launch_tris_bound(c, tris, dirs, T, (int)budget, amax, cellW, bin_log2(c)));
+    c->samp_n = (int)budget;
+    c->samp_amax = amax;
+    s = voxelize_common(c, tris, dirs, T, cellW, emit_sampled_tris);
+    c->samp_amax = nullptr;
+    dfree(c, amax);
     timer_end(c, c->t_vox);
     return s;
 }

@@ -158,6 +158,8 @@ struct vox_ctx {
     unsigned long long* d_counter = nullptr; // pair cursor
     vox_stats st{};
     std::string err;
+    int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
+    const unsigned* samp_amax = nullptr;    // device max triangle area bits of the call (§12)
     int dmode = 0;                          // 0 sigma distance, 1 histogram distance (§10)
     int hist_n = 5000;                      // samples per histogram (§10)
     float* d_hist_u = nullptr;              // [3][N] sample table (SoA); process-wide, not owned
@@ -203,6 +205,16 @@ void upload_theta(vox_ctx* c);
 // histogram distance (k_hist.cu)
 void host_hist_tables(int N, std::vector<float>& u, std::vector<uint8_t>& permT, std::vector<uint32_t>& gapT);
 cudaError_t upload_hist_tables(vox_ctx* c);
+// sampling front end (k_sample.cu)
+cudaError_t launch_spline_bound(vox_ctx* c, const float* ctrl, const float* rad, uint64_t S, int n,
+                                unsigned long long* cellW, int bin_log2);
+cudaError_t launch_spline_emit(vox_ctx* c, const float* ctrl, const float* rad, uint64_t S, int n, Shard sh,
+                               Bins bins, uint64_t* keys, uint64_t* vals, float4* ptab);
+cudaError_t launch_tris_bound(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, int budget,
+                              unsigned* amax_bits, unsigned long long* cellW, int bin_log2);
+cudaError_t launch_tris_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, int budget,
+                             const unsigned* amax_bits, Shard sh, Bins bins, uint64_t* keys, uint64_t* vals,
+                             float4* ptab);
 // compact form (k_encode.cu)
 cudaError_t launch_encode(vox_ctx* c, const Level& L, int leaf, uint8_t* out6, uint8_t* cl6, uint8_t* flags);
 cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
