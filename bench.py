@@ -174,6 +174,9 @@ def main():
     ap.add_argument("--distance", default="sigma", choices=["sigma", "hist"],
                     help="SGGX-H distance: sigma (PREDICATES §9) or the paper's histogram distance (§10)")
     ap.add_argument("--hist-samples", type=int, default=5000, help="N samples per SGGX histogram (P:389)")
+    ap.add_argument("--sampled", type=int, default=0,
+                    help="N > 0: the paper's sampling front end (PREDICATES §12), N samples per Catmull-Rom "
+                         "piece (fibers) or N samples for the largest triangle, instead of exact overlap")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-finalize", action="store_true", help="skip the compact-form (NEXT-3) measurement")
@@ -205,6 +208,9 @@ def main():
         h_a, h_b = c["segments"], c["radii"]
     else:
         h_a, h_b = c["tris"], c["dirs"]
+    if args.sampled and fib:
+        import gen as _gen
+        h_a = _gen.splines_from_segments(h_a)      # Catmull-Rom controls [S,4,3] of the same fibers
     n_prims = len(h_a)
     d_a = torch.from_numpy(h_a).cuda()
     d_b = torch.from_numpy(h_b).cuda() if h_b is not None else None
@@ -213,7 +219,12 @@ def main():
     def step(profile=False):
         v = Vox(N, bbox, rank=rank, world=world, profile=profile, distance=args.distance,
                 hist_samples=args.hist_samples)
-        if fib:
+        if args.sampled:
+            if fib:
+                v.sample_splines(d_a, d_b, args.sampled)
+            else:
+                v.sample_triangles(d_a, d_b, args.sampled)
+        elif fib:
             v.voxelize_fibers(d_a, d_b)
         else:
             v.voxelize_triangles(d_a, d_b)
@@ -278,8 +289,10 @@ def main():
     bytes_lod = sum((36 * V[0] if l == 1 else 121 * V[l - 1]) + 121 * V[l] for l in range(1, levels + 1))
     sig_ev, dist_ev = lodwork["sigma"] / args.steps, lodwork["dist"] / args.steps
     flops_sggxh = 416.0 * sig_ev + 95.0 * dist_ev      # PREDICATES §9: 32 x 13 per sigma, 32+32+31 per distance
+    emit_name = ("k_spline_emit" if fib else "k_tris_emit") if args.sampled else ("k_fiber_emit" if fib else "k_tri_emit")
+    emit_bytes = (52 * n_prims + 32 * P) if (args.sampled and fib) else (28 * n_prims + 16 * P + 16 * n_prims)
     kern = {
-        ("k_fiber_emit" if fib else "k_tri_emit"): (stage["ms_emit"], "hbm", 28 * n_prims + 16 * P + 16 * n_prims),
+        emit_name: (stage["ms_emit"], "hbm", emit_bytes),
         "k_bin_count": (stage["ms_sort"], "hbm", 8 * P),
         "k_bin_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
         "k_lod_prep": (stage["ms_lod_prep"], "hbm", bytes_lod),
@@ -318,6 +331,9 @@ def main():
             "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config]
                        + (f" [point: {n_prims} segments at {N}^3]" if args.config == 5 else ""),
                        "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
+                       "front_end": (f"sampled ({args.sampled} samples per Catmull-Rom piece)" if fib else
+                                     f"sampled (budget {args.sampled} per largest triangle)") if args.sampled
+                       else "exact overlap",
                        "sggxh_distance": args.distance if args.distance == "sigma"
                        else f"hist (N={args.hist_samples} samples, 5x5x5 bins, sliced W1)",
                        "l2": "inputs (28 B x prims) larger than L2; no flush"},
@@ -329,7 +345,7 @@ def main():
             "sggxh_work": {"sigma_evals": sig_ev, "dist_evals": dist_ev, "hard_parents": lodwork["hard"] / args.steps}}
 
     # ---------------------------------------------------------------- e2e through the C ABI, host buffers
-    if not args.no_e2e:
+    if not args.no_e2e and not args.sampled:
         pa = torch.from_numpy(h_a).pin_memory()
         pb = torch.from_numpy(h_b).pin_memory() if h_b is not None else None
         outs = {}
@@ -398,7 +414,7 @@ def main():
         del bufs
 
     # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and fib:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and fib and not args.sampled:
         lvl = 9 if N >= 4096 else max(1, int(math.log2(N)) - 3)
         target = args.cpu_segments if args.distance == "sigma" else max(1000, args.cpu_segments // 100)
         n, dt, desc = oracle_sample(c, target, lvl, args.distance, args.hist_samples)
