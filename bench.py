@@ -320,10 +320,29 @@ def main():
                  "alg_flops_per_launch": work}
         r["frac"] = (r["achieved"] / r["peak"]) if r["achieved"] else None
         r["ms_per_launch"] = ms_k
-        r["traffic"] = None
+        r["traffic"] = traffic.get(name)
+        if r["traffic"] is not None:
+            r["traffic_source"] = f"{traffic_src}: dram__bytes_read.sum + dram__bytes_write.sum, all launches of one step"
         return r
+    # traffic: DRAM bytes per step of the same kernels from the committed ncu launch list of this
+    # workload (profiles/rNN_traffic.json, tools/profile_round.sh); null for other workloads
+    groups = {"k_sggxh_quad+half+warp": ["k_sggxh_quad", "k_sggxh_half", "k_sggxh_warp"],
+              "k_fiber_emit": ["k_fiber_emit"], "k_bin_count": ["k_bin_count"],
+              "k_bin_reduce": ["k_bin_reduce", "k_bin_reduce_warp"],
+              "k_lod_prep": ["k_lod_prep", "k_lod_prep_leaf"]}
+    traffic, traffic_src = {}, None
+    if args.config == 4 and not args.segments and not args.sampled and args.distance == "sigma":
+        import glob
+        tf = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+        if tf:
+            tj = json.load(open(tf[-1]))
+            traffic_src = os.path.relpath(tf[-1], ROOT)
+            for g, ks in groups.items():
+                if all(k in tj for k in ks):
+                    traffic[g] = sum(tj[k]["dram_bytes"] for k in ks)
     roof = roof_of(dom)
-    others = {k: {kk: roof_of(k)[kk] for kk in ("bound", "achieved", "unit", "frac", "ms_per_launch")} for k in kern}
+    others = {k: {kk: roof_of(k)[kk] for kk in ("bound", "achieved", "unit", "frac", "ms_per_launch", "traffic")}
+              for k in kern}
 
     line = {"metric": METRIC, "value": value, "unit": "segments/s" if fib else "triangles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
