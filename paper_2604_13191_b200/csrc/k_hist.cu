@@ -139,8 +139,9 @@ __device__ __forceinline__ void hist_build(const long long* lob, const float* __
 // d_hist(i, j_q) for up to 4 rows j_q at once (PREDICATES §10): lane k walks slice k, the
 // table and H_i loads shared by the rows; exact 64-bit warp sums
 template <int R>
-__device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* const (&Hj)[4], const uint8_t* permT,
-                                           const uint32_t* gapT, int lane, unsigned long long (&out)[4]) {
+__device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* const (&Hj)[4],
+                                           const uint32_t* __restrict__ pg, int lane,
+                                           unsigned long long (&out)[4]) {
     int C[R];
     unsigned long long W[R];
 #pragma unroll
@@ -150,8 +151,9 @@ __device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* c
     }
 #pragma unroll 2
     for (int r = 0; r < HR; r++) {
-        const int b = permT[r * 32 + lane];
-        const unsigned g = gapT[r * 32 + lane];
+        const unsigned w = __ldg(pg + r * 32 + lane);   // (gap << 8) | cell, L1-resident
+        const int b = (int)(w & 0xffu);
+        const unsigned g = w >> 8;
         const int hi = Hi[b];
 #pragma unroll
         for (int q = 0; q < R; q++) {
@@ -169,13 +171,13 @@ __device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* c
 
 // distances of row i to the listed columns xs[0..m-1] (m <= 4), batched
 __device__ __forceinline__ void hist_row4(const uint16_t (*H)[128], int i, const int (&xs)[4], int m,
-                                          const uint8_t* permT, const uint32_t* gapT, int lane,
+                                          const uint32_t* __restrict__ pg, int lane,
                                           unsigned long long (&out)[4]) {
     const uint16_t* Hj[4] = {H[xs[0]], H[xs[m > 1 ? 1 : 0]], H[xs[m > 2 ? 2 : 0]], H[xs[m > 3 ? 3 : 0]]};
-    if (m == 4) hist_pairs<4>(H[i], Hj, permT, gapT, lane, out);
-    else if (m == 3) hist_pairs<3>(H[i], Hj, permT, gapT, lane, out);
-    else if (m == 2) hist_pairs<2>(H[i], Hj, permT, gapT, lane, out);
-    else hist_pairs<1>(H[i], Hj, permT, gapT, lane, out);
+    if (m == 4) hist_pairs<4>(H[i], Hj, pg, lane, out);
+    else if (m == 3) hist_pairs<3>(H[i], Hj, pg, lane, out);
+    else if (m == 2) hist_pairs<2>(H[i], Hj, pg, lane, out);
+    else hist_pairs<1>(H[i], Hj, pg, lane, out);
 }
 
 // key = (d << 16) | (i << 8) | j orders by (d, i, j); d < 2^38 (32 slices x N x 2^20)
@@ -189,7 +191,7 @@ struct HistSmem {
     static constexpr int MAXN = 8 * K;
     static constexpr int MAXP = MAXN * (MAXN - 1) / 2;
     static constexpr int WARPS = K <= 4 ? 4 : 2;
-    static constexpr size_t tables = HR * 32 + HR * 32 * 4;                  // perm u8 + gap u32
+    static constexpr size_t tables = 0;   // slice tables are read from global memory (L1)
     static constexpr size_t lob_bytes = MAXN * 7 * 8;
     static constexpr size_t H_bytes = MAXN * 128 * 2;
     static constexpr size_t priv_bytes = HB * 32;
@@ -204,17 +206,10 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
              const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
              uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
-             const float* __restrict__ hu, int N, const uint8_t* __restrict__ gperm,
-             const uint32_t* __restrict__ ggap) {
+             const float* __restrict__ hu, int N, const uint32_t* __restrict__ gpg) {
     using SM = HistSmem<K>;
     constexpr int MAXN = SM::MAXN;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint8_t* permT = smem_raw;
-    uint32_t* gapT = reinterpret_cast<uint32_t*>(smem_raw + HR * 32);
-    for (int x = threadIdx.x; x < HR * 8; x += blockDim.x)
-        reinterpret_cast<uint32_t*>(permT)[x] = reinterpret_cast<const uint32_t*>(gperm)[x];
-    for (int x = threadIdx.x; x < HR * 32; x += blockDim.x) gapT[x] = ggap[x];
-    __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned char* base = smem_raw + SM::tables + wib * SM::per_warp;
     long long(*lob)[7] = reinterpret_cast<long long(*)[7]>(base);
@@ -267,7 +262,7 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 const int m = n - j0 < 4 ? n - j0 : 4;
                 const int xs[4] = {j0, j0 + 1, j0 + 2, j0 + 3};
                 unsigned long long d[4];
-                hist_row4(H, i, xs, m, permT, gapT, lane, d);
+                hist_row4(H, i, xs, m, gpg, lane, d);
                 if (lane < m) {
                     const int j = j0 + lane;
                     const unsigned long long dv = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
@@ -303,7 +298,7 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                             m++;
                         }
                     unsigned long long d[4];
-                    hist_row4(H, bi, xs, m, permT, gapT, lane, d);
+                    hist_row4(H, bi, xs, m, gpg, lane, d);
                     if (lane < m) {
                         const int x = lane == 0 ? xs[0] : lane == 1 ? xs[1] : lane == 2 ? xs[2] : xs[3];
                         const unsigned long long dv = lane == 0 ? d[0] : lane == 1 ? d[1] : lane == 2 ? d[2] : d[3];
@@ -346,7 +341,7 @@ static cudaError_t launch_hist_k(vox_ctx* c, const uint32_t* list, const unsigne
     nb = std::min<uint64_t>(std::max<uint64_t>(nb, 1), 148ull * 8);
     k_sggxh_hist<K><<<(unsigned)nb, SM::WARPS * 32, SM::total, c->stream>>>(
         list, counts, C.acc, C.ncl, C.clacc, leaf, start, P.ncl, P.clacc, P.cl, c->d_hist_u, c->hist_n,
-        c->d_hist_perm, c->d_hist_gap);
+        c->d_hist_pg);
     return cudaGetLastError();
 }
 
@@ -368,8 +363,7 @@ cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const uns
 // pool): creating a ctx in the histogram mode costs no host table work or copies after that.
 struct HistTablesDev {
     float* u = nullptr;
-    uint8_t* perm = nullptr;
-    uint32_t* gap = nullptr;
+    uint32_t* pg = nullptr;   // [124][32] (gap << 8) | cell
 };
 static std::mutex g_hist_mu;
 static std::map<std::pair<int, int>, HistTablesDev> g_hist_tables;
@@ -386,19 +380,18 @@ cudaError_t upload_hist_tables(vox_ctx* c) {
         std::vector<uint8_t> perm;
         std::vector<uint32_t> gap;
         host_hist_tables(c->hist_n, u, perm, gap);
+        std::vector<uint32_t> pg(perm.size());
+        for (size_t x = 0; x < pg.size(); x++) pg[x] = (gap[x] << 8) | perm[x];   // gaps < 2^20
         HistTablesDev t;
         if ((e = cudaMalloc((void**)&t.u, u.size() * 4)) != cudaSuccess) return e;
-        if ((e = cudaMalloc((void**)&t.perm, perm.size())) != cudaSuccess) return e;
-        if ((e = cudaMalloc((void**)&t.gap, gap.size() * 4)) != cudaSuccess) return e;
+        if ((e = cudaMalloc((void**)&t.pg, pg.size() * 4)) != cudaSuccess) return e;
         // synchronous copies from pageable host vectors (once per process, device and N)
         if ((e = cudaMemcpy(t.u, u.data(), u.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-        if ((e = cudaMemcpy(t.perm, perm.data(), perm.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-        if ((e = cudaMemcpy(t.gap, gap.data(), gap.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+        if ((e = cudaMemcpy(t.pg, pg.data(), pg.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
         T = t;
     }
     c->d_hist_u = T.u;
-    c->d_hist_perm = T.perm;
-    c->d_hist_gap = T.gap;
+    c->d_hist_pg = T.pg;
     return cudaSuccess;
 }
 

@@ -163,8 +163,7 @@ struct vox_ctx {
     int dmode = 0;                          // 0 sigma distance, 1 histogram distance (§10)
     int hist_n = 5000;                      // samples per histogram (§10)
     float* d_hist_u = nullptr;              // [3][N] sample table (SoA); process-wide, not owned
-    uint8_t* d_hist_perm = nullptr;         // [124][32] sorted bins per slice (transposed)
-    uint32_t* d_hist_gap = nullptr;         // [124][32] fixed-point gaps (transposed)
+    uint32_t* d_hist_pg = nullptr;          // [124][32] (gap << 8) | cell of each slice step (transposed)
     // stage timers (profile = 1)
     vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp, t_encode;
 };
