@@ -370,15 +370,19 @@ def main():
         outs = {}
         host = {}
 
+        copy_stream = torch.cuda.Stream()
+
         def e2e_step():
             v = Vox(N, bbox, rank=rank, world=world, distance=args.distance, hist_samples=args.hist_samples)
             if fib:
                 v.voxelize_fibers_host(pa, pb)
             else:
                 v.voxelize_triangles_host(pa, pb)
-            v.build_lod(levels, group)
             d2h = 0
-            for l in range(1, levels + 1):   # the LoD volumes delivered to host memory (levels 1..L)
+            # build level by level; each finished level's D2H runs on a second stream while the
+            # next levels are built (vox_copy_level_async: event-ordered, no sync)
+            for l in range(1, levels + 1):
+                v.build_lod(l, group)
                 n_l = int(v.view(l)["n"])
                 if l not in host or host[l]["key"].numel() < n_l:
                     host[l] = {"key": torch.empty(n_l, dtype=torch.int64).pin_memory(),
@@ -386,8 +390,9 @@ def main():
                                "m6": torch.empty(n_l * 6, dtype=torch.float32).pin_memory(),
                                "ncl": torch.empty(n_l, dtype=torch.uint8).pin_memory(),
                                "cl": torch.empty(n_l * v.k * 7, dtype=torch.float32).pin_memory()}
-                v.copy_level_to(l, host[l])
+                v.copy_level_async(l, host[l], copy_stream)
                 d2h += n_l * (8 + 4 + 24 + 1 + 28 * v.k)
+            copy_stream.synchronize()
             v.close()
             outs["d2h"] = d2h
 

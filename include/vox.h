@@ -162,6 +162,15 @@ vox_status vox_sample_triangles(vox_ctx* ctx, const float* tris, const float* di
  * level > built -> VOX_ERR_LEVEL; sggx6 NULL -> VOX_ERR_INVALID_ARG. */
 vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags);
 
+/* Like vox_copy_level but asynchronous on the caller's `stream` (a cudaStream_t, NULL = the
+ * legacy default stream): the copies are ordered after the work already enqueued on the ctx
+ * stream (an event), and the call returns without synchronising, so the D2H of level l
+ * overlaps the build of levels > l. Building further levels does not touch lower levels;
+ * the caller synchronises `stream` before reading the buffers or destroying the ctx.
+ * Level 0 supports key / mass / m6 only (ncl or cl non-NULL -> VOX_ERR_INVALID_ARG). */
+vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
+                                uint8_t* ncl, float* cl, void* stream);
+
 /* Copy a level's exact accumulators acc [n][7] (int64, quantum 2^-32; device or host). */
 vox_status vox_copy_level_acc(vox_ctx* ctx, uint32_t level, int64_t* acc);
 

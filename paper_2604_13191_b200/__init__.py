@@ -78,6 +78,7 @@ def lib():
     L.vox_read_level.argtypes = [vp, u32, C.POINTER(_View)]
     L.vox_copy_level.argtypes = [vp, u32, vp, vp, vp, vp, vp]
     L.vox_copy_level_acc.argtypes = [vp, u32, vp]
+    L.vox_copy_level_async.argtypes = [vp, u32, vp, vp, vp, vp, vp, vp]
     L.vox_encode_level.argtypes = [vp, u32, vp, vp, vp]
     L.vox_sample_splines.argtypes = [vp, vp, vp, u64, u32]
     L.vox_sample_triangles.argtypes = [vp, vp, vp, u64, u32]
@@ -97,7 +98,7 @@ def lib():
     L.vox_destroy.argtypes = [vp]
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
-                 "vox_copy_level", "vox_copy_level_acc", "vox_encode_level", "vox_sample_splines",
+                 "vox_copy_level", "vox_copy_level_acc", "vox_copy_level_async", "vox_encode_level", "vox_sample_splines",
                  "vox_sample_triangles", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
@@ -318,6 +319,15 @@ class Vox:
         self._check(lib().vox_encode_level(self._h, int(level), ptr("sggx6"), ptr("cl6"), ptr("flags")),
                     "encode_level")
         return {k: t[:n] for k, t in out.items()}
+
+    def copy_level_async(self, level: int, out: dict, stream):
+        """vox_copy_level_async: enqueue the copy of a level into caller tensors (pinned host or
+        device; keys key/mass/m6/ncl/cl, each optional) on `stream` (torch.cuda.Stream), ordered
+        after the ctx's work so far; no synchronisation."""
+        ptr = lambda k: out[k].data_ptr() if k in out and out[k] is not None else None
+        self._check(lib().vox_copy_level_async(self._h, int(level), ptr("key"), ptr("mass"), ptr("m6"),
+                                               ptr("ncl"), ptr("cl"), C.c_void_p(stream.cuda_stream)),
+                    "copy_level_async")
 
     # ------------------------------------------------------------------ multi-GPU records
     def export_level(self, level: int):

@@ -617,6 +617,28 @@ vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass
     return VOX_OK;
 }
 
+vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float* mass, float* m6, uint8_t* ncl,
+                                float* cl, void* stream) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    if (level == 0 && (ncl || cl)) return VOX_ERR_INVALID_ARG;
+    const Level& L = c->lv[level];
+    const uint64_t n = L.n;
+    if (n == 0) return VOX_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t ev;
+    CKS(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CKS(cudaEventRecord(ev, c->stream));      // after everything that produced the level
+    CKS(cudaStreamWaitEvent(s, ev, 0));
+    CKS(cudaEventDestroy(ev));
+    if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, s));
+    if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, s));
+    if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, s));
+    if (ncl) CKS(cudaMemcpyAsync(ncl, L.ncl, n, cudaMemcpyDefault, s));
+    if (cl) CKS(cudaMemcpyAsync(cl, L.cl, n * c->K * 28, cudaMemcpyDefault, s));
+    return VOX_OK;
+}
+
 vox_status vox_copy_level_acc(vox_ctx* c, uint32_t level, int64_t* acc) {
     if (!c || !acc) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;

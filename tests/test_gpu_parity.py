@@ -118,6 +118,26 @@ def test_host_entry_points(P):
     o.build(6)
     for l in range(7):
         _cmp_level(v.level(l, device="cpu"), o.level(l), l, "host")
+    # asynchronous D2H on a side stream, interleaved with the build of further levels
+    w = P.Vox(c["grid_res"], c["bbox"])
+    w.voxelize_triangles_host(c["tris"])
+    side = torch.cuda.Stream()
+    outs = {}
+    for l in range(1, 7):
+        w.build_lod(l)
+        n = int(w.view(l)["n"])
+        outs[l] = {"key": torch.empty(n, dtype=torch.int64).pin_memory(),
+                   "mass": torch.empty(n, dtype=torch.float32).pin_memory(),
+                   "m6": torch.empty((n, 6), dtype=torch.float32).pin_memory(),
+                   "ncl": torch.empty(n, dtype=torch.uint8).pin_memory(),
+                   "cl": torch.empty((n, 3, 7), dtype=torch.float32).pin_memory()}
+        w.copy_level_async(l, outs[l], side)
+    side.synchronize()
+    for l in range(1, 7):
+        r = o.level(l)
+        assert np.array_equal(outs[l]["key"].numpy().astype(np.uint64), r["key"])
+        assert np.array_equal(outs[l]["mass"].numpy(), r["mass"]) and np.array_equal(outs[l]["m6"].numpy(), r["m6"])
+        assert np.array_equal(outs[l]["ncl"].numpy(), r["ncl"]) and np.array_equal(outs[l]["cl"].numpy(), r["cl"])
 
 
 def test_errors_and_states(P):
