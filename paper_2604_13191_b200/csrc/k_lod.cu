@@ -1060,8 +1060,7 @@ vox_status build_level(vox_ctx* c, int l) {
     CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
     c->st.launches += 2;
     uint32_t V = 0;
-    CK(cudaMemcpyAsync(&V, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(ssync(c));
+    CK(readback(c, {{&V, incl + n - 1, 4}}));
     CK(dalloc(c, (void**)&start, ((uint64_t)V + 1) * 4));
     k_pstarts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
     c->st.launches++;
@@ -1158,8 +1157,7 @@ vox_status unpack_level(vox_ctx* c, int level, const void* buf, uint64_t n) {
                                                  c->d_flags);
     c->st.launches++;
     unsigned fl = 0;
-    CK(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(ssync(c));
+    CK(readback(c, {{&fl, c->d_flags, 4}}));
     if (fl) {
         c->err = "import: records not strictly ascending or bad lobe count";
         free_level(c, L);

@@ -80,8 +80,7 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
     c->st.launches += 2;   // scan init + scan
     uint32_t V32 = 0;
-    CK(cudaMemcpyAsync(&V32, incl + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(ssync(c));
+    CK(readback(c, {{&V32, incl + n - 1, 4}}));
     CK(dalloc(c, (void**)&start, ((uint64_t)V32 + 1) * 4));
     k_starts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
     c->st.launches++;
@@ -538,8 +537,7 @@ vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigne
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, caps, off, (int64_t)(nb + 1), c->stream));
     c->st.launches += 3;
     unsigned long long cap = 0;
-    CK(cudaMemcpyAsync(&cap, off + nb, 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(ssync(c));
+    CK(readback(c, {{&cap, off + nb, 8}}));
     dfree(c, tmp);
     dfree(c, caps);
     *off_out = off;
@@ -575,9 +573,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     c->st.launches += 4;
     unsigned V = 0;
     unsigned long long P = 0;
-    CK(cudaMemcpyAsync(&V, voff + nb, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(&P, npairs, 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(ssync(c));
+    CK(readback(c, {{&V, voff + nb, 4}, {&P, npairs, 8}}));
     timer_end(c, c->t_sort);
     c->st.pairs = P;
     timer_begin(c, c->t_reduce);

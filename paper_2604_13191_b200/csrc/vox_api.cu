@@ -101,6 +101,65 @@ cudaError_t ssync(vox_ctx* c) {
     return e;
 }
 
+// Small device->host reads (counts, flags) without the copy engines: a one-block kernel
+// copies the words into host-mapped pinned memory, then the ctx stream is synchronised. A
+// cudaMemcpyAsync would queue behind large D2H transfers the caller may have in flight on
+// another stream (vox_copy_level_async) and serialise the build with them.
+__global__ void k_peek(const unsigned* __restrict__ src, unsigned* __restrict__ dst, int nwords) {
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+}
+
+static std::mutex g_map_mu;
+static std::vector<std::pair<void*, void*>> g_map_pool;   // (host, device) mapped pinned blocks
+constexpr size_t MAP_BYTES = 64 * 1024;
+
+static cudaError_t acquire_mapped(vox_ctx* c) {
+    if (c->h_map) return cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        if (!g_map_pool.empty()) {
+            c->h_map = g_map_pool.back().first;
+            c->d_map = g_map_pool.back().second;
+            g_map_pool.pop_back();
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaHostAlloc(&c->h_map, MAP_BYTES, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    return cudaHostGetDevicePointer(&c->d_map, c->h_map, 0);
+}
+
+static void release_mapped(vox_ctx* c) {
+    if (!c->h_map) return;
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    g_map_pool.push_back({c->h_map, c->d_map});
+    c->h_map = c->d_map = nullptr;
+}
+
+cudaError_t readback(vox_ctx* c, std::initializer_list<ReadItem> items) {
+    cudaError_t e = acquire_mapped(c);
+    if (e != cudaSuccess) return e;
+    size_t off = 0;
+    for (const ReadItem& it : items) {
+        const size_t words = (it.bytes + 3) / 4;
+        if ((off + words) * 4 > MAP_BYTES) return cudaErrorInvalidValue;
+        k_peek<<<1, 256, 0, c->stream>>>(reinterpret_cast<const unsigned*>(it.src),
+                                         reinterpret_cast<unsigned*>(c->d_map) + off, (int)words);
+        off += words;
+    }
+    c->st.launches += items.size();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = ssync(c);
+    if (e != cudaSuccess) return e;
+    off = 0;
+    for (const ReadItem& it : items) {
+        std::memcpy(it.dst, reinterpret_cast<const unsigned*>(c->h_map) + off, it.bytes);
+        off += (it.bytes + 3) / 4;
+    }
+    return cudaSuccess;
+}
+
 void free_level(vox_ctx* c, Level& L) {
     dfree(c, L.key); dfree(c, L.acc); dfree(c, L.mass); dfree(c, L.m6);
     dfree(c, L.ncl); dfree(c, L.clacc); dfree(c, L.cl);
@@ -290,8 +349,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     const uint64_t ncells = ncells_of(c), nb = nbins_of(c);
     const int Lb = bin_log2(c);
     unsigned fl = 0;
-    CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CKS(ssync(c));
+    CKS(readback(c, {{&fl, c->d_flags, 4}}));
     timer_end(c, c->t_bound);
     if (fl) {
         dfree(c, Wb);
@@ -363,8 +421,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     CKS(emit(c, a, b, n, sh, bins, keys, vals, ptab));
     timer_end(c, c->t_emit);
     s = reduce_bins(c, keys, vals, bins, nb, ptab);
-    CKS(cudaMemcpyAsync(&fl, c->d_flags, 4, cudaMemcpyDeviceToHost, c->stream));
-    CKS(ssync(c));
+    CKS(readback(c, {{&fl, c->d_flags, 4}}));
     dfree(c, keys);
     dfree(c, vals);
     dfree(c, ptab);
@@ -719,7 +776,7 @@ vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     c->st.ms_encode = timer_flush(c, c->t_encode);
     if (c->d_lodwork) {
         unsigned long long w[3] = {0, 0, 0};
-        CKS(cudaMemcpy(w, c->d_lodwork, 24, cudaMemcpyDeviceToHost));
+        CKS(readback(c, {{w, c->d_lodwork, 24}}));
         c->st.lod_sigma_evals = w[0];
         c->st.lod_dist_evals = w[1];
         c->st.lod_hard_parents = w[2];
@@ -759,6 +816,7 @@ vox_status vox_sync(vox_ctx* c) {
 void vox_destroy(vox_ctx* c) {
     if (!c) return;
     ssync(c);
+    release_mapped(c);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
                           &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode}) {

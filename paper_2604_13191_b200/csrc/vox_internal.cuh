@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -158,6 +159,8 @@ struct vox_ctx {
     unsigned long long* d_counter = nullptr; // pair cursor
     vox_stats st{};
     std::string err;
+    void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
+    void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
     const unsigned* samp_amax = nullptr;    // device max triangle area bits of the call (§12)
     int dmode = 0;                          // 0 sigma distance, 1 histogram distance (§10)
@@ -173,6 +176,13 @@ namespace vox {
 // allocation helpers (stream-ordered)
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes);
 cudaError_t ssync(vox_ctx* c);   // cudaStreamSynchronize with host-time accounting
+struct ReadItem {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+// small device->host reads through host-mapped memory (no copy engine), then a stream sync
+cudaError_t readback(vox_ctx* c, std::initializer_list<ReadItem> items);
 void dfree(vox_ctx* c, void* p);
 void vox_trim_stream(cudaStream_t s);   // release the allocation cache of a stream
 void free_level(vox_ctx* c, Level& L);
