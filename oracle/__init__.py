@@ -79,6 +79,9 @@ def lib():
         L.orc_encode.argtypes = [C.c_uint64, i64p, u8p, u8p]
         L.orc_finalize.argtypes = [i64p, f32p]
         L.orc_spline_eval.argtypes = [f32p, C.c_float, f32p, f32p]
+        L.orc_density_fibers.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64]
+        L.orc_density_triangles.argtypes = [C.c_void_p, f32p, C.c_uint64]
+        L.orc_density_level.argtypes = [C.c_void_p, C.c_int, u64p, f32p, f32p]
         L.orc_sample_splines.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64, C.c_int]
         L.orc_sample_triangles.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64, C.c_int]
         L.orc_tri_samples.argtypes = [C.c_float, C.c_float, C.c_int]
@@ -161,6 +164,25 @@ class Oracle:
         if dirs is not None:
             d, dp = _f32(np.asarray(dirs).reshape(-1, 3))
         _check(lib().orc_sample_triangles(self._h, tp, dp, t.shape[0], int(budget)), "sample_triangles")
+
+    def density_fibers(self, segments, radii):
+        """§13: OR the sub-voxel hits of fiber segments into the level-0 masks (after build)."""
+        s, sp = _f32(np.asarray(segments).reshape(-1, 6))
+        r, rp = _f32(np.asarray(radii).reshape(-1))
+        _check(lib().orc_density_fibers(self._h, sp, rp, s.shape[0]), "density_fibers")
+
+    def density_triangles(self, tris):
+        t, tp = _f32(np.asarray(tris).reshape(-1, 9))
+        _check(lib().orc_density_triangles(self._h, tp, t.shape[0]), "density_triangles")
+
+    def density_level(self, l: int) -> dict:
+        """§13 masks [n,8] uint64 (word z, bit x + 8 y), occupancy [n], axis [n,3] (YZ, XZ, XY)."""
+        n = int(lib().orc_level_size(self._h, int(l)))
+        out = dict(mask=np.zeros((n, 8), np.uint64), occ=np.zeros(n, np.float32), axis=np.zeros((n, 3), np.float32))
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        _check(lib().orc_density_level(self._h, int(l), P(out["mask"], C.c_uint64), P(out["occ"], C.c_float),
+                                       P(out["axis"], C.c_float)), "density_level")
+        return out
 
     def build(self, levels: int = 0):
         _check(lib().orc_build(self._h, int(levels)), "build")

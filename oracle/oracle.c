@@ -395,6 +395,8 @@ typedef struct {
     int mode;                 /* 0: sigma distance (§9), 1: histogram distance (§10) */
     int hist_n;               /* N samples per histogram (§10) */
     struct hist_tables* ht;   /* §10 tables (mode 1) */
+    uint64_t* dm0;            /* §13 level-0 sub-voxel masks [lv[0].n][8] (NULL: none) */
+    uint64_t dm0_n;
 } orc_ctx;
 
 static int hist_tables_init(hist_tables_t* T, int N);
@@ -455,6 +457,7 @@ void orc_destroy(orc_ctx* c) {
     free_levels(c);
     free(c->recs);
     if (c->ht) { free(c->ht->u); free(c->ht); }
+    free(c->dm0);
     free(c);
 }
 
@@ -786,6 +789,154 @@ int orc_sample_triangles(orc_ctx* c, const float* tri, const float* dirs, uint64
             if (rc) return rc;
         }
     }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ §13 sub-voxel density */
+/* The paper's occupancy and axis-projected densities:
+ * Res_3 = 8 sub-voxels per voxel edge; sub-voxel (a,b,c) of voxel (i,j,k) is hit iff the key
+ * predicate of §4 / §6 holds for the fine voxel (8i+a, 8j+b, 8k+c) with grid-space geometry
+ * scaled by 8 (exactly the key predicate of an 8N grid). Masks are OR-ed over primitives. */
+static int64_t key_index(const level_t* L, uint64_t key) {
+    int64_t lo = 0, hi = (int64_t)L->n - 1;
+    while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (L->key[mid] == key) return mid;
+        if (L->key[mid] < key) lo = mid + 1;
+        else hi = mid - 1;
+    }
+    return -1;
+}
+
+static int density_prepare(orc_ctx* c) {
+    if (c->built < 0) return ORC_ERR_LEVEL;
+    if (!c->dm0 || c->dm0_n != c->lv[0].n) {
+        free(c->dm0);
+        c->dm0_n = c->lv[0].n;
+        c->dm0 = (uint64_t*)calloc((c->dm0_n ? c->dm0_n : 1) * 8, sizeof(uint64_t));
+        if (!c->dm0) return ORC_ERR_OOM;
+    }
+    return ORC_OK;
+}
+
+static void density_set(orc_ctx* c, int64_t x, int64_t y, int64_t z) {
+    int64_t v = key_index(&c->lv[0], orc_morton((uint32_t)(x >> 3), (uint32_t)(y >> 3), (uint32_t)(z >> 3)));
+    if (v < 0) return; /* a fine hit outside the key set (possible only by rounding): dropped */
+    c->dm0[8 * v + (z & 7)] |= 1ull << ((x & 7) + 8 * (y & 7));
+}
+
+/* fine candidate range of one axis, clamped to the grid and the window */
+static int fine_range(const orc_ctx* c, int ax, float lo, float hi, int64_t* f0, int64_t* f1) {
+    int64_t N8 = 8 * (int64_t)c->g.N;
+    if (!(hi >= -1.0f) || !(lo <= (float)N8 + 1.0f)) return 0;
+    cand_range(lo, hi, f0, f1);
+    int64_t w0 = 8 * c->wlo[ax], w1 = 8 * c->whi[ax] + 7;
+    if (*f0 < w0) *f0 = w0;
+    if (*f1 > w1) *f1 = w1;
+    if (*f0 < 0) *f0 = 0;
+    if (*f1 > N8 - 1) *f1 = N8 - 1;
+    return *f0 <= *f1;
+}
+
+int orc_density_fibers(orc_ctx* c, const float* seg, const float* radii, uint64_t S) {
+    int rc = density_prepare(c);
+    if (rc) return rc;
+    for (uint64_t p = 0; p < S; p++) {
+        float a[3], b[3];
+        for (int ax = 0; ax < 3; ax++) {
+            a[ax] = 8.0f * grid_coord(&c->g, ax, seg[6 * p + ax]);
+            b[ax] = 8.0f * grid_coord(&c->g, ax, seg[6 * p + 3 + ax]);
+        }
+        float rg = 8.0f * grid_len(&c->g, radii[p]);
+        int64_t f0[3], f1[3];
+        int ok = 1;
+        for (int ax = 0; ax < 3; ax++) {
+            float lo = fminf_(a[ax], b[ax]) - rg, hi = fmaxf_(a[ax], b[ax]) + rg;
+            if (!fine_range(c, ax, lo, hi, &f0[ax], &f1[ax])) ok = 0;
+        }
+        if (!ok) continue;
+        if ((f1[0] - f0[0] + 1) * (f1[1] - f0[1] + 1) * (f1[2] - f0[2] + 1) > (1ll << 26)) return ORC_ERR_ARG;
+        fiber_t f;
+        fiber_setup(&f, a, b, rg);
+        for (int64_t z = f0[2]; z <= f1[2]; z++)
+            for (int64_t y = f0[1]; y <= f1[1]; y++)
+                for (int64_t x = f0[0]; x <= f1[0]; x++) {
+                    float ell;
+                    if (fiber_eval(&f, x, y, z, &ell)) density_set(c, x, y, z);
+                }
+    }
+    return ORC_OK;
+}
+
+int orc_density_triangles(orc_ctx* c, const float* tri, uint64_t T) {
+    int rc = density_prepare(c);
+    if (rc) return rc;
+    for (uint64_t t = 0; t < T; t++) {
+        float g[9];
+        for (int q = 0; q < 9; q++) g[q] = 8.0f * grid_coord(&c->g, q % 3, tri[9 * t + q]);
+        int64_t f0[3], f1[3];
+        int ok = 1;
+        for (int ax = 0; ax < 3; ax++) {
+            float lo = fminf_(fminf_(g[ax], g[3 + ax]), g[6 + ax]);
+            float hi = fmaxf_(fmaxf_(g[ax], g[3 + ax]), g[6 + ax]);
+            if (!fine_range(c, ax, lo, hi, &f0[ax], &f1[ax])) ok = 0;
+        }
+        if (!ok) continue;
+        if ((f1[0] - f0[0] + 1) * (f1[1] - f0[1] + 1) * (f1[2] - f0[2] + 1) > (1ll << 26)) return ORC_ERR_ARG;
+        for (int64_t z = f0[2]; z <= f1[2]; z++)
+            for (int64_t y = f0[1]; y <= f1[1]; y++)
+                for (int64_t x = f0[0]; x <= f1[0]; x++)
+                    if (tri_sat(g, x, y, z)) density_set(c, x, y, z);
+    }
+    return ORC_OK;
+}
+
+/* Masks of level l (direct from level 0: a level-0 sub-voxel at fine offset X inside a
+ * level-l voxel lands in the level-l sub-voxel X >> l), occupancy = hits / 512 and
+ * the coverage of the projections onto the YZ, XZ, XY planes / 64. */
+int orc_density_level(const orc_ctx* c, int l, uint64_t* masks, float* occ, float* axis) {
+    if (l < 0 || l > c->built || !c->dm0) return ORC_ERR_LEVEL;
+    const level_t* L = &c->lv[l];
+    uint64_t* m = (uint64_t*)calloc((L->n ? L->n : 1) * 8, sizeof(uint64_t));
+    if (!m) return ORC_ERR_OOM;
+    const level_t* L0 = &c->lv[0];
+    for (uint64_t v = 0; v < L0->n; v++) {
+        uint32_t i, j, k;
+        orc_unmorton(L0->key[v], &i, &j, &k);
+        int64_t pv = key_index(L, L0->key[v] >> (3 * l));
+        if (pv < 0) continue;
+        uint32_t span = 1u << l;
+        for (int cz = 0; cz < 8; cz++)
+            for (int cy = 0; cy < 8; cy++)
+                for (int cx = 0; cx < 8; cx++) {
+                    if (!((c->dm0[8 * v + cz] >> (cx + 8 * cy)) & 1ull)) continue;
+                    uint32_t X = 8 * (i % span) + cx, Y = 8 * (j % span) + cy, Z = 8 * (k % span) + cz;
+                    uint32_t A = X >> l, B = Y >> l, C = Z >> l;
+                    m[8 * pv + C] |= 1ull << (A + 8 * B);
+                }
+    }
+    for (uint64_t v = 0; v < L->n; v++) {
+        const uint64_t* w = m + 8 * v;
+        uint64_t xy = 0, hits = 0, xz = 0, yz = 0;
+        for (int cz = 0; cz < 8; cz++) {
+            xy |= w[cz];
+            hits += (uint64_t)__builtin_popcountll(w[cz]);
+            for (int cy = 0; cy < 8; cy++)
+                for (int cx = 0; cx < 8; cx++)
+                    if ((w[cz] >> (cx + 8 * cy)) & 1ull) {
+                        xz |= 1ull << (cx + 8 * cz);
+                        yz |= 1ull << (cy + 8 * cz);
+                    }
+        }
+        if (masks) memcpy(masks + 8 * v, w, 64);
+        if (occ) occ[v] = (float)hits / 512.0f;
+        if (axis) {
+            axis[3 * v + 0] = (float)__builtin_popcountll(yz) / 64.0f;
+            axis[3 * v + 1] = (float)__builtin_popcountll(xz) / 64.0f;
+            axis[3 * v + 2] = (float)__builtin_popcountll(xy) / 64.0f;
+        }
+    }
+    free(m);
     return ORC_OK;
 }
 
