@@ -87,6 +87,7 @@ typedef struct {
     uint64_t lod_sigma_evals, lod_dist_evals, lod_hard_parents;
     double host_ms_alloc, host_ms_sync;   /* host time in stream-ordered allocation / stream syncs */
     double ms_encode;      /* vox_encode_level device time (profile=1) */
+    double ms_density;     /* vox_density_* device time (profile=1) */
 } vox_stats;
 
 /* Create a ctx for an N^3 grid over the cubic extent of bbox (D3).
@@ -148,6 +149,22 @@ vox_status vox_copy_level(vox_ctx* ctx, uint32_t level, uint64_t* key, float* ma
  * Non-finite input, negative radius or zero dirs -> VOX_ERR_INVALID_ARG at the call's sync. */
 vox_status vox_sample_splines(vox_ctx* ctx, const float* ctrl, const float* radii, uint64_t S, uint32_t n);
 vox_status vox_sample_triangles(vox_ctx* ctx, const float* tris, const float* dirs, uint64_t T, uint32_t budget);
+
+/* Sub-voxel occupancy and axis-projected densities (PREDICATES §13; P:282-291, P:347-349,
+ * S:266-271). Res_3 = 8: sub-voxel (a,b,c) of voxel (i,j,k) is hit iff
+ * the key predicate (§4 fibers / §6 triangles) holds for fine voxel (8i+a, 8j+b, 8k+c) of the
+ * 8N grid. vox_density_fibers / _triangles OR the hits of the given primitives (device
+ * arrays as in vox_voxelize_*) into per-voxel 512-bit masks of level 0; call them after the
+ * last voxelize call (a voxelize call resets the masks), once per primitive batch.
+ * Before any voxelize call -> VOX_ERR_STATE. Inputs are assumed validated by voxelize.
+ * vox_density_level(level): occ [n] = hits / 512, axis [n][3] = projected coverage onto the
+ * YZ, XZ, XY planes / 64, masks [n][8] (word z, bit x + 8 y; NULL = skipped) into caller
+ * device buffers; level > 0 masks are the 2x2x2 OR-downsampling of level - 1 (built lazily).
+ * No masks yet -> VOX_ERR_STATE; level > built -> VOX_ERR_LEVEL; sharded ctx: levels above
+ * log2(N) - T -> VOX_ERR_STATE (masks are not exchanged). */
+vox_status vox_density_fibers(vox_ctx* ctx, const float* segments, const float* radii, uint64_t S);
+vox_status vox_density_triangles(vox_ctx* ctx, const float* tris, uint64_t T);
+vox_status vox_density_level(vox_ctx* ctx, uint32_t level, float* occ, float* axis, uint64_t* masks);
 
 /* SGGX finalisation and the 6-byte compact form (PREDICATES §11; Eq. compact-sggx P:354-362,
  * SPEC S:47) of every record of a level, into

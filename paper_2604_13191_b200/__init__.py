@@ -53,7 +53,7 @@ class _Stats(C.Structure):
                 ("ms_sggxh_half", C.c_double), ("ms_sggxh_warp", C.c_double),
                 ("launches", C.c_uint64), ("lod_sigma_evals", C.c_uint64), ("lod_dist_evals", C.c_uint64),
                 ("lod_hard_parents", C.c_uint64), ("host_ms_alloc", C.c_double), ("host_ms_sync", C.c_double),
-                ("ms_encode", C.c_double)]
+                ("ms_encode", C.c_double), ("ms_density", C.c_double)]
 
 
 _lib = None
@@ -81,6 +81,9 @@ def lib():
     L.vox_copy_level_async.argtypes = [vp, u32, vp, vp, vp, vp, vp, vp]
     L.vox_encode_level.argtypes = [vp, u32, vp, vp, vp]
     L.vox_sample_splines.argtypes = [vp, vp, vp, u64, u32]
+    L.vox_density_fibers.argtypes = [vp, vp, vp, u64]
+    L.vox_density_triangles.argtypes = [vp, vp, u64]
+    L.vox_density_level.argtypes = [vp, u32, vp, vp, vp]
     L.vox_sample_triangles.argtypes = [vp, vp, vp, u64, u32]
     L.vox_export_level.argtypes = [vp, u32, vp, C.POINTER(u64)]
     L.vox_import_level.argtypes = [vp, u32, vp, u64]
@@ -99,7 +102,7 @@ def lib():
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
                  "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
                  "vox_copy_level", "vox_copy_level_acc", "vox_copy_level_async", "vox_encode_level", "vox_sample_splines",
-                 "vox_sample_triangles", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
+                 "vox_sample_triangles", "vox_density_fibers", "vox_density_triangles", "vox_density_level", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
         getattr(L, name).restype = i32
     _lib = L
@@ -303,6 +306,30 @@ class Vox:
         d = None if dirs is None else _dev_f32(dirs, "dirs", (3,))
         self._check(lib().vox_sample_triangles(self._h, t.data_ptr(), None if d is None else d.data_ptr(),
                                                t.shape[0], int(budget)), "sample_triangles")
+
+    def density_fibers(self, segments, radii):
+        """vox_density_fibers (PREDICATES §13): OR the sub-voxel hits of fiber segments into the
+        level-0 masks (after the last voxelize call)."""
+        s = _dev_f32(segments, "segments", (2, 3))
+        r = _dev_f32(radii, "radii", ())
+        self._check(lib().vox_density_fibers(self._h, s.data_ptr(), r.data_ptr(), s.shape[0]), "density_fibers")
+
+    def density_triangles(self, tris):
+        t = _dev_f32(tris, "tris", (3, 3))
+        self._check(lib().vox_density_triangles(self._h, t.data_ptr(), t.shape[0]), "density_triangles")
+
+    def density_level(self, level: int, masks: bool = False) -> dict:
+        """vox_density_level: occupancy [n] and axis densities [n,3] (YZ, XZ, XY) as cuda
+        tensors, plus the 512-bit masks [n,8] (int64 bit patterns) when masks=True."""
+        import torch
+        n = int(self.view(level)["n"])
+        out = {"occ": torch.empty(max(n, 1), dtype=torch.float32, device="cuda"),
+               "axis": torch.empty((max(n, 1), 3), dtype=torch.float32, device="cuda")}
+        if masks:
+            out["mask"] = torch.empty((max(n, 1), 8), dtype=torch.int64, device="cuda")
+        self._check(lib().vox_density_level(self._h, int(level), out["occ"].data_ptr(), out["axis"].data_ptr(),
+                                            out["mask"].data_ptr() if masks else None), "density_level")
+        return {k: t[:n] for k, t in out.items()}
 
     def encode_level(self, level: int, lobes: bool = True, flags: bool = True) -> dict:
         """vox_encode_level (PREDICATES §11): the 6-byte compact SGGX of every voxel

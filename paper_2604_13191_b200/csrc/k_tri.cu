@@ -337,4 +337,77 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
     return e;
 }
 
+// ---------------------------------------------------------------- §13 sub-voxel density
+// Warp per triangle: key voxels by the §6 SAT, then per key voxel the 512 sub-voxels (16 per
+// lane) by the §6 SAT on the 8x grid, skipping (no hit) sub-voxels whose centre is farther
+// than sqrt(3)/2 + 0.25 fine voxels from the triangle's plane (GPU-only shortcut; the pinned
+// SAT cannot report overlap there).
+__global__ void __launch_bounds__(256)
+k_tri_density(const float* __restrict__ tri, uint64_t T, GridXf gx, const uint64_t* __restrict__ keys0,
+              uint64_t n0, unsigned long long* __restrict__ masks) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarp = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = warp; t < T; t += nwarp) {
+        float v[9];
+        for (int q = 0; q < 9; q++) v[q] = tri[9 * t + q];
+        TriGeom G;
+        tri_geom(gx, v, G);
+        if (G.culled) continue;
+        float g8[9];
+        for (int q = 0; q < 9; q++) g8[q] = 8.0f * G.g[q];
+        // plane of the fine triangle (shortcut geometry only)
+        float e1[3], e2[3], n[3];
+        for (int ax = 0; ax < 3; ax++) {
+            e1[ax] = g8[3 + ax] - g8[ax];
+            e2[ax] = g8[6 + ax] - g8[ax];
+        }
+        cross3(e1, e2, n);
+        const float nn = sqrtf(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        const float lim = 1.11602540378f * nn;   // (sqrt(3)/2 + 0.25) |n|
+        const int64_t ex = G.e1[0] - G.e0[0] + 1, ey = G.e1[1] - G.e0[1] + 1, ez = G.e1[2] - G.e0[2] + 1;
+        const int64_t ncand = ex * ey * ez;
+        for (int64_t base = 0; base < ncand; base += 32) {
+            const int64_t cidx = base + lane;
+            int64_t i = 0, j = 0, k = 0;
+            bool key = false;
+            if (cidx < ncand) {
+                i = G.e0[0] + cidx % ex;
+                j = G.e0[1] + (cidx / ex) % ey;
+                k = G.e0[2] + cidx / (ex * ey);
+                key = tri_box_sat(G.g, i, j, k);
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, key);
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const int64_t vi = __shfl_sync(0xffffffffu, i, src), vj = __shfl_sync(0xffffffffu, j, src),
+                              vk = __shfl_sync(0xffffffffu, k, src);
+                long long idx = -1;
+                if (lane == 0) idx = find_key(keys0, n0, morton3((uint32_t)vi, (uint32_t)vj, (uint32_t)vk));
+                idx = __shfl_sync(0xffffffffu, idx, 0);
+                if (idx < 0) continue;
+                unsigned hb[16];
+#pragma unroll
+                for (int q = 0; q < 16; q++) {
+                    const int sub = lane + 32 * q;
+                    const int64_t x = 8 * vi + (sub & 7), y = 8 * vj + ((sub >> 3) & 7), z = 8 * vk + (sub >> 6);
+                    const float pd = (((float)x + 0.5f) - g8[0]) * n[0] + (((float)y + 0.5f) - g8[1]) * n[1] +
+                                     (((float)z + 0.5f) - g8[2]) * n[2];
+                    const bool hit = (nn > 0.0f && fabsf(pd) > lim) ? false : tri_box_sat(g8, x, y, z);
+                    hb[q] = __ballot_sync(0xffffffffu, hit);
+                }
+                or_mask16(hb, idx, lane, masks);
+            }
+        }
+    }
+}
+
+cudaError_t launch_tri_density(vox_ctx* c, const float* tri, uint64_t T) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((T + 7) / 8, 148ull * 16);
+    k_tri_density<<<grid ? grid : 1, 256, 0, c->stream>>>(tri, T, c->g, c->lv[0].key, c->lv[0].n, c->dmask[0]);
+    c->st.launches++;
+    return cudaGetLastError();
+}
+
 }  // namespace vox

@@ -343,8 +343,11 @@ typedef cudaError_t (*emit_fn)(vox_ctx*, const float*, const float*, uint64_t, S
 static int bin_log2(const vox_ctx* c) { return std::min(c->g.logN >= 13 ? 5 : 4, c->g.logN - c->T); }
 static uint64_t nbins_of(const vox_ctx* c) { return 1ull << (3 * (c->g.logN - bin_log2(c))); }
 
+static void density_reset(vox_ctx* c);
+
 static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, uint64_t n, unsigned long long* Wb,
                                   emit_fn emit, uint64_t nptab = 0) {
+    density_reset(c);   // level 0 changes: sub-voxel masks must be recomputed (vox_density_*)
     if (nptab == 0) nptab = n;   // prim-table entries (one per sample for the spline front end)
     const uint64_t ncells = ncells_of(c), nb = nbins_of(c);
     const int Lb = bin_log2(c);
@@ -634,6 +637,80 @@ __global__ void k_leaf_lobes(uint64_t n, const float* __restrict__ mass, const f
     }
 }
 
+// ---------------------------------------------------------------- §13 sub-voxel density
+static void density_reset(vox_ctx* c) {
+    for (int l = 0; l < VOX_MAX_LEVELS; l++)
+        if (c->dmask[l]) {
+            dfree(c, c->dmask[l]);
+            c->dmask[l] = nullptr;
+        }
+    c->dmask_levels = -1;
+}
+
+static vox_status density_prepare(vox_ctx* c) {
+    if (c->state == ST_CREATED || c->built < 0) return VOX_ERR_STATE;
+    for (int l = 1; l < VOX_MAX_LEVELS; l++)   // lower-level masks change: rebuild upper ones lazily
+        if (c->dmask[l]) {
+            dfree(c, c->dmask[l]);
+            c->dmask[l] = nullptr;
+        }
+    if (!c->dmask[0]) {
+        const uint64_t n0 = c->lv[0].n;
+        CKS(dalloc(c, (void**)&c->dmask[0], (n0 ? n0 : 1) * 64));
+        CKS(cudaMemsetAsync(c->dmask[0], 0, (n0 ? n0 : 1) * 64, c->stream));
+    }
+    c->dmask_levels = 0;
+    return VOX_OK;
+}
+
+vox_status vox_density_fibers(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (S && (!segments || !radii)) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    s = density_prepare(c);
+    if (s != VOX_OK) return s;
+    if (S == 0 || c->lv[0].n == 0) return VOX_OK;
+    timer_begin(c, c->t_density);
+    CKS(launch_fiber_density(c, segments, radii, S));
+    timer_end(c, c->t_density);
+    return VOX_OK;
+}
+
+vox_status vox_density_triangles(vox_ctx* c, const float* tris, uint64_t T) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (T && !tris) return VOX_ERR_INVALID_ARG;
+    vox_status s = ensure_dev(c);
+    if (s != VOX_OK) return s;
+    s = density_prepare(c);
+    if (s != VOX_OK) return s;
+    if (T == 0 || c->lv[0].n == 0) return VOX_OK;
+    timer_begin(c, c->t_density);
+    CKS(launch_tri_density(c, tris, T));
+    timer_end(c, c->t_density);
+    return VOX_OK;
+}
+
+vox_status vox_density_level(vox_ctx* c, uint32_t level, float* occ, float* axis, uint64_t* masks) {
+    if (!c) return VOX_ERR_INVALID_ARG;
+    if (c->dmask_levels < 0) return VOX_ERR_STATE;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    if (c->world > 1 && (int)level > c->g.logN - c->T) return VOX_ERR_STATE;   // masks are not exchanged
+    timer_begin(c, c->t_density);
+    for (int l = c->dmask_levels + 1; l <= (int)level; l++) {
+        const uint64_t n = c->lv[l].n;
+        CKS(dalloc(c, (void**)&c->dmask[l], (n ? n : 1) * 64));
+        CKS(cudaMemsetAsync(c->dmask[l], 0, (n ? n : 1) * 64, c->stream));
+        CKS(launch_density_down(c, l));
+        c->dmask_levels = l;
+    }
+    if (occ || axis) CKS(launch_density_stats(c, (int)level, occ, axis));
+    if (masks && c->lv[level].n)
+        CKS(cudaMemcpyAsync(masks, c->dmask[level], c->lv[level].n * 64, cudaMemcpyDefault, c->stream));
+    timer_end(c, c->t_density);
+    return VOX_OK;
+}
+
 vox_status vox_encode_level(vox_ctx* c, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags) {
     if (!c || !sggx6) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
@@ -774,6 +851,7 @@ vox_status vox_stats_get(vox_ctx* c, vox_stats* out) {
     c->st.ms_sggxh_half = timer_flush(c, c->t_half);
     c->st.ms_sggxh_warp = timer_flush(c, c->t_warp);
     c->st.ms_encode = timer_flush(c, c->t_encode);
+    c->st.ms_density = timer_flush(c, c->t_density);
     if (c->d_lodwork) {
         unsigned long long w[3] = {0, 0, 0};
         CKS(readback(c, {{w, c->d_lodwork, 24}}));
@@ -790,7 +868,7 @@ vox_status vox_stats_reset(vox_ctx* c) {
     vox_stats tmp;
     vox_stats_get(c, &tmp);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode})
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode, &c->t_density})
         t->ms = 0.0;
     c->st.launches = 0;
     c->st.host_ms_alloc = c->st.host_ms_sync = 0;
@@ -817,9 +895,10 @@ void vox_destroy(vox_ctx* c) {
     if (!c) return;
     ssync(c);
     release_mapped(c);
+    density_reset(c);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
-                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode}) {
+                          &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode, &c->t_density}) {
         timer_flush(c, *t);
         if (t->open) cudaEventDestroy(t->open);
     }

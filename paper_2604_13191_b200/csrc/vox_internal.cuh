@@ -115,6 +115,30 @@ __device__ __forceinline__ void append_binned(bool emit, uint64_t mkey, uint64_t
     }
 }
 
+// §13 sub-voxel density: index of `key` in a sorted key array (-1 if absent)
+__device__ __forceinline__ long long find_key(const uint64_t* __restrict__ keys, uint64_t n, uint64_t key) {
+    long long lo = 0, hi = (long long)n - 1;
+    while (lo <= hi) {
+        const long long mid = (lo + hi) >> 1;
+        const uint64_t k = keys[mid];
+        if (k == key) return mid;
+        if (k < key) lo = mid + 1;
+        else hi = mid - 1;
+    }
+    return -1;
+}
+
+// §13: ORs a voxel's 512-bit hit mask, given as 16 warp ballots (ballot q covers sub-voxels
+// lane + 32 q, i.e. word q >> 1, bits 32 (q & 1) + lane), into masks[idx][0..7]. Warp-wide.
+__device__ __forceinline__ void or_mask16(const unsigned (&bal)[16], long long idx, int lane,
+                                          unsigned long long* __restrict__ masks) {
+    unsigned long long w = 0;
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+        if ((q >> 1) == lane) w |= (unsigned long long)bal[q] << (32 * (q & 1));
+    if (lane < 8 && w) atomicOr(&masks[8 * idx + lane], w);
+}
+
 // ---------------------------------------------------------------- host-side state
 
 struct Level {
@@ -159,6 +183,8 @@ struct vox_ctx {
     unsigned long long* d_counter = nullptr; // pair cursor
     vox_stats st{};
     std::string err;
+    unsigned long long* dmask[VOX_MAX_LEVELS] = {};   // §13 sub-voxel masks per level ([n][8]), lazily
+    int dmask_levels = -1;                  // levels with valid masks (0 after vox_density_*)
     void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
     void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
@@ -168,7 +194,7 @@ struct vox_ctx {
     float* d_hist_u = nullptr;              // [3][N] sample table (SoA); process-wide, not owned
     uint32_t* d_hist_pg = nullptr;          // [124][32] (gap << 8) | cell of each slice step (transposed)
     // stage timers (profile = 1)
-    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp, t_encode;
+    vox::StageTimer t_bound, t_emit, t_sort, t_reduce, t_merge, t_lodscan, t_lod, t_vox, t_lodall, t_prep, t_quad, t_half, t_warp, t_encode, t_density;
 };
 
 namespace vox {
@@ -224,6 +250,11 @@ cudaError_t launch_tris_bound(vox_ctx* c, const float* tri, const float* dirs, u
 cudaError_t launch_tris_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, int budget,
                              const unsigned* amax_bits, Shard sh, Bins bins, uint64_t* keys, uint64_t* vals,
                              float4* ptab);
+// sub-voxel density (k_fiber.cu, k_tri.cu, k_density.cu)
+cudaError_t launch_fiber_density(vox_ctx* c, const float* seg, const float* rad, uint64_t S);
+cudaError_t launch_tri_density(vox_ctx* c, const float* tri, uint64_t T);
+cudaError_t launch_density_down(vox_ctx* c, int level);   // masks of `level` from level - 1
+cudaError_t launch_density_stats(vox_ctx* c, int level, float* occ, float* axis);
 // compact form (k_encode.cu)
 cudaError_t launch_encode(vox_ctx* c, const Level& L, int leaf, uint8_t* out6, uint8_t* cl6, uint8_t* flags);
 cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
