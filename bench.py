@@ -434,6 +434,17 @@ def main():
         line["finalize"] = {"ms": st["ms_encode"], "records": recs, "records_per_s": recs / (st["ms_encode"] / 1e3),
                             "alg_bytes": byts, "achieved_gbs": byts / (st["ms_encode"] / 1e3) / 1e9,
                             "bound": "alu (pinned Jacobi: ~18 rotations with IEEE div/sqrt per record)"}
+        # NEXT-2: sub-voxel occupancy and axis densities of every level (same ctx, after the build)
+        if fib and not args.sampled:
+            v.stats_reset()
+            v.density_fibers(d_a, d_b)
+            dens = [v.density_level(l) for l in range(levels + 1)]
+            st = v.stats()
+            line["density"] = {"ms": st["ms_density"], "leaf_voxels": V[0],
+                               "sub_voxel_tests_per_leaf": 512,
+                               "leaf_voxels_per_s": V[0] / (st["ms_density"] / 1e3),
+                               "bound": "alu (pinned capsule-box predicate on the 8N grid for boundary sub-voxels)"}
+            del dens
         v.close()
         del bufs
 

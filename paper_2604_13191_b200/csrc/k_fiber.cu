@@ -410,8 +410,11 @@ __device__ __forceinline__ void fib_setup(Fib& f, float (&d)[3], const float* a,
     f.len = sqrtf(ss);
 }
 
-// centre distance^2 of fine voxel (x,y,z) to the segment (GPU-only shortcut geometry)
-__device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, int64_t x, int64_t y, int64_t z) {
+// centre distance^2 of fine voxel (x,y,z) to the segment, and (box2) the squared distance from
+// the segment point nearest the centre to the box (GPU-only shortcut geometry: the
+// segment-box distance lies in [sqrt(c2) - sqrt(3)/2, sqrt(box2)])
+__device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, int64_t x, int64_t y, int64_t z,
+                                              float& box2) {
     const float e0 = ((float)x + 0.5f) - f.a[0], e1 = ((float)y + 0.5f) - f.a[1], e2 = ((float)z + 0.5f) - f.a[2];
     const float ww = f.w[0] + f.w[1] + f.w[2];
     float t = 0.0f;
@@ -420,19 +423,23 @@ __device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, int6
         t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
     }
     const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
+    const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f), o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
+    box2 = o0 * o0 + o1 * o1 + o2 * o2;
     return q0 * q0 + q1 * q1 + q2 * q2;
 }
 
 // Warp per segment: its key voxels (the §4 predicate, as in emit), and for each key voxel the
 // 512 sub-voxels, 16 per lane: the §4 predicate on the 8x grid, with conservative shortcuts
-// (centre farther than R + sqrt(3)/2 + 0.25 fine voxels: no hit; nearer than R - 0.25: hit,
-// since the centre lies in the box) that the pinned fp32 decision cannot contradict (its deviation
+// (centre farther than R + sqrt(3)/2 + 0.25 fine voxels: no hit; the box within R - 0.25 of
+// the segment point nearest its centre: hit) that the pinned fp32 decision cannot contradict (its deviation
 // from the exact one is < 0.02 fine voxels at 8N <= 65536). The mask of each key voxel is
 // OR-ed into the level-0 masks (a key absent from level 0 = another shard: skipped).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g,
                 const uint64_t* __restrict__ keys0, uint64_t n0, unsigned long long* __restrict__ masks) {
-    const int lane = threadIdx.x & 31;
+    __shared__ unsigned s_m[8][16];        // per warp: the voxel's 512-bit mask
+    __shared__ uint16_t s_q[8][512];       // per warp: undecided sub-voxels
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarp = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t p = warp; p < S; p += nwarp) {
@@ -476,22 +483,39 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                 if (lane == 0) idx = find_key(keys0, n0, morton3((uint32_t)vi, (uint32_t)vj, (uint32_t)vk));
                 idx = __shfl_sync(0xffffffffu, idx, 0);
                 if (idx < 0) continue;
-                unsigned hb[16];
-#pragma unroll
+                // classify the 512 sub-voxels (16 per lane): sure hits straight into the mask,
+                // undecided ones queued, then the queue evaluated 32 at a time (no divergence)
+                int nq = 0;
+#pragma unroll 1
                 for (int q = 0; q < 16; q++) {
                     const int sub = lane + 32 * q;
                     const int64_t x = 8 * vi + (sub & 7), y = 8 * vj + ((sub >> 3) & 7), z = 8 * vk + (sub >> 6);
-                    const float c2 = centre_dist2(f8, d8, x, y, z);
-                    bool hit;
-                    if (c2 > far2) hit = false;
-                    else if (c2 < near2) hit = true;
-                    else {
-                        float ell;
-                        hit = fiber_key(f8, x, y, z, ell);
-                    }
-                    hb[q] = __ballot_sync(0xffffffffu, hit);
+                    float box2;
+                    const float c2 = centre_dist2(f8, d8, x, y, z, box2);
+                    const bool sure = box2 < near2, open = !sure && !(c2 > far2);
+                    const unsigned bs = __ballot_sync(0xffffffffu, sure);
+                    const unsigned bo = __ballot_sync(0xffffffffu, open);
+                    if (lane == 0) s_m[wib][q] = bs;
+                    if (open) s_q[wib][nq + __popc(bo & ((1u << lane) - 1u))] = (uint16_t)sub;
+                    nq += __popc(bo);
                 }
-                or_mask16(hb, idx, lane, masks);
+                __syncwarp();
+#pragma unroll 1
+                for (int b0 = 0; b0 < nq; b0 += 32) {
+                    if (b0 + lane < nq) {
+                        const int sub = s_q[wib][b0 + lane];
+                        float ell;
+                        if (fiber_key(f8, 8 * vi + (sub & 7), 8 * vj + ((sub >> 3) & 7), 8 * vk + (sub >> 6), ell))
+                            atomicOr(&s_m[wib][sub >> 5], 1u << (sub & 31));
+                    }
+                }
+                __syncwarp();
+                if (lane < 8) {
+                    const unsigned long long word =
+                        (unsigned long long)s_m[wib][2 * lane] | ((unsigned long long)s_m[wib][2 * lane + 1] << 32);
+                    if (word) atomicOr(&masks[8 * idx + lane], word);
+                }
+                __syncwarp();
             }
         }
     }

@@ -342,10 +342,12 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
 // lane) by the §6 SAT on the 8x grid, skipping (no hit) sub-voxels whose centre is farther
 // than sqrt(3)/2 + 0.25 fine voxels from the triangle's plane (GPU-only shortcut; the pinned
 // SAT cannot report overlap there).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_tri_density(const float* __restrict__ tri, uint64_t T, GridXf gx, const uint64_t* __restrict__ keys0,
               uint64_t n0, unsigned long long* __restrict__ masks) {
-    const int lane = threadIdx.x & 31;
+    __shared__ unsigned s_m[8][16];        // per warp: the voxel's 512-bit mask
+    __shared__ uint16_t s_q[8][512];       // per warp: sub-voxels to test
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarp = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t t = warp; t < T; t += nwarp) {
@@ -387,17 +389,37 @@ k_tri_density(const float* __restrict__ tri, uint64_t T, GridXf gx, const uint64
                 if (lane == 0) idx = find_key(keys0, n0, morton3((uint32_t)vi, (uint32_t)vj, (uint32_t)vk));
                 idx = __shfl_sync(0xffffffffu, idx, 0);
                 if (idx < 0) continue;
-                unsigned hb[16];
-#pragma unroll
+                // sub-voxels off the plane's slab are no hit; the others are queued and tested
+                // by the pinned SAT 32 at a time
+                int nq = 0;
+                if (lane < 16) s_m[wib][lane] = 0u;
+#pragma unroll 1
                 for (int q = 0; q < 16; q++) {
                     const int sub = lane + 32 * q;
                     const int64_t x = 8 * vi + (sub & 7), y = 8 * vj + ((sub >> 3) & 7), z = 8 * vk + (sub >> 6);
                     const float pd = (((float)x + 0.5f) - g8[0]) * n[0] + (((float)y + 0.5f) - g8[1]) * n[1] +
                                      (((float)z + 0.5f) - g8[2]) * n[2];
-                    const bool hit = (nn > 0.0f && fabsf(pd) > lim) ? false : tri_box_sat(g8, x, y, z);
-                    hb[q] = __ballot_sync(0xffffffffu, hit);
+                    const bool open = !(nn > 0.0f && fabsf(pd) > lim);
+                    const unsigned bo = __ballot_sync(0xffffffffu, open);
+                    if (open) s_q[wib][nq + __popc(bo & ((1u << lane) - 1u))] = (uint16_t)sub;
+                    nq += __popc(bo);
                 }
-                or_mask16(hb, idx, lane, masks);
+                __syncwarp();
+#pragma unroll 1
+                for (int b0 = 0; b0 < nq; b0 += 32) {
+                    if (b0 + lane < nq) {
+                        const int sub = s_q[wib][b0 + lane];
+                        if (tri_box_sat(g8, 8 * vi + (sub & 7), 8 * vj + ((sub >> 3) & 7), 8 * vk + (sub >> 6)))
+                            atomicOr(&s_m[wib][sub >> 5], 1u << (sub & 31));
+                    }
+                }
+                __syncwarp();
+                if (lane < 8) {
+                    const unsigned long long word =
+                        (unsigned long long)s_m[wib][2 * lane] | ((unsigned long long)s_m[wib][2 * lane + 1] << 32);
+                    if (word) atomicOr(&masks[8 * idx + lane], word);
+                }
+                __syncwarp();
             }
         }
     }

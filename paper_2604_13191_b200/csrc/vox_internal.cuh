@@ -128,17 +128,6 @@ __device__ __forceinline__ long long find_key(const uint64_t* __restrict__ keys,
     return -1;
 }
 
-// §13: ORs a voxel's 512-bit hit mask, given as 16 warp ballots (ballot q covers sub-voxels
-// lane + 32 q, i.e. word q >> 1, bits 32 (q & 1) + lane), into masks[idx][0..7]. Warp-wide.
-__device__ __forceinline__ void or_mask16(const unsigned (&bal)[16], long long idx, int lane,
-                                          unsigned long long* __restrict__ masks) {
-    unsigned long long w = 0;
-#pragma unroll
-    for (int q = 0; q < 16; q++)
-        if ((q >> 1) == lane) w |= (unsigned long long)bal[q] << (32 * (q & 1));
-    if (lane < 8 && w) atomicOr(&masks[8 * idx + lane], w);
-}
-
 // ---------------------------------------------------------------- host-side state
 
 struct Level {
