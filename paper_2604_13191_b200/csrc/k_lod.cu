@@ -408,6 +408,11 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     __shared__ __align__(16) float s_cf[32][6];
     for (int x = threadIdx.x; x < 32 * 6; x += blockDim.x) s_cf[x / 6][x % 6] = c_coef[x / 6][x % 6];
     __syncthreads();
+    float2 cf[4][3];   // coefficients of this lane's slices l, l+8, l+16, l+24
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int e = 0; e < 3; e++) cf[q][e] = reinterpret_cast<const float2*>(s_cf[l + 8 * q])[e];
     const unsigned small = counts[0];
     const unsigned nquad = (small + 3) / 4;
     for (unsigned qd = blockIdx.x * QUAD_WARPS + wib; qd < nquad; qd += gridDim.x * QUAD_WARPS) {
@@ -476,24 +481,25 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         for (int c = 0; c < 8; c++)
 #pragma unroll
             for (int q = 0; q < 4; q++) sg[c][q] = 0.0f;
+        // lobe-outer: each lobe's S row is read once and used for the lane's 4 slices
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const float2* cfr = reinterpret_cast<const float2*>(s_cf[l + 8 * q]);
-            const float2 c01 = cfr[0], c23 = cfr[1], c45 = cfr[2];
+        for (int c = 0; c < 8; c++) {
+            if (c >= nmax) break;
+            float2 s01 = make_float2(0.0f, 0.0f), s23 = s01, s45 = s01;
+            if (valid && c < n) {
+                const float2* sr = reinterpret_cast<const float2*>(Sg[c]);
+                s01 = sr[0];
+                s23 = sr[1];
+                s45 = sr[2];
+            }
 #pragma unroll
-            for (int c = 0; c < 8; c++) {
-                if (c >= nmax) break;
-                float qq = 0.0f;
-                if (valid && c < n) {
-                    const float2* sr = reinterpret_cast<const float2*>(Sg[c]);
-                    const float2 s01 = sr[0], s23 = sr[1], s45 = sr[2];
-                    qq = c01.x * s01.x;
-                    qq = qq + c01.y * s01.y;
-                    qq = qq + c23.x * s23.x;
-                    qq = qq + c23.y * s23.y;
-                    qq = qq + c45.x * s45.x;
-                    qq = qq + c45.y * s45.y;
-                }
+            for (int q = 0; q < 4; q++) {
+                float qq = cf[q][0].x * s01.x;
+                qq = qq + cf[q][0].y * s01.y;
+                qq = qq + cf[q][1].x * s23.x;
+                qq = qq + cf[q][1].y * s23.y;
+                qq = qq + cf[q][2].x * s45.x;
+                qq = qq + cf[q][2].y * s45.y;
                 sg[c][q] = sqrtf(pmax(qq, 0.0f));
             }
         }
@@ -528,14 +534,21 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (act && l < 6) Sg[bi][l] = deq32(lobe[bi][1 + l]) / deq32(lobe[bi][0]);
             __syncwarp();
             float sn[4];
+            float2 m01 = make_float2(0.0f, 0.0f), m23 = m01, m45 = m01;
+            if (act) {
+                const float2* sr = reinterpret_cast<const float2*>(Sg[bi]);
+                m01 = sr[0];
+                m23 = sr[1];
+                m45 = sr[2];
+            }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                float qq = 0.0f;
-                if (act) {
-                    qq = s_cf[l + 8 * q][0] * Sg[bi][0];
-#pragma unroll
-                    for (int e = 1; e < 6; e++) qq = qq + s_cf[l + 8 * q][e] * Sg[bi][e];
-                }
+                float qq = cf[q][0].x * m01.x;
+                qq = qq + cf[q][0].y * m01.y;
+                qq = qq + cf[q][1].x * m23.x;
+                qq = qq + cf[q][1].y * m23.y;
+                qq = qq + cf[q][2].x * m45.x;
+                qq = qq + cf[q][2].y * m45.y;
                 sn[q] = sqrtf(pmax(qq, 0.0f));
             }
 #pragma unroll
