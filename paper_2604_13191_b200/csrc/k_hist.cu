@@ -285,6 +285,7 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (lane < 7) lob[bi][lane] += lob[bj][lane];   // exact moment merge (D15)
             alive &= ~(1ull << bj);
             __syncwarp();
+            if (m == K + 1) break;   // the last merge: no histogram or distance is read afterwards
             hist_build(lob[bi], ux, uy, uz, N, priv, H[bi], lane);   // fresh histogram of the merged S
             {   // new row d(bi, x) for the live x, four at a time
                 unsigned long long rest = alive & ~(1ull << bi);

@@ -280,9 +280,11 @@ __global__ void k_bucket_init(const unsigned* __restrict__ hist, int K, int maxn
         off += hist[n];
         if (n <= 8) small = off;
         if (n <= 16) mid = off;
+        // evaluations actually needed: n initial sigmas and pairs, then a new sigma and a new
+        // row for every merge but the last (after it, nothing reads sigma or D)
         unsigned long long d = (unsigned long long)n * (n - 1) / 2;
-        for (int m = n; m > K; m--) d += (unsigned long long)(m - 2);
-        sg += (unsigned long long)hist[n] * (unsigned long long)(2 * n - K);
+        for (int m = n; m > K + 1; m--) d += (unsigned long long)(m - 2);
+        sg += (unsigned long long)hist[n] * (unsigned long long)(2 * n - K - 1);
         dd += (unsigned long long)hist[n] * d;
         hp += hist[n];
     }
@@ -531,6 +533,10 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             const int bi = (int)((best >> 8) & 0xff), bj = (int)(best & 0xff);
             if (act && l < 7) lobe[bi][l] += lobe[bj][l];   // exact moment merge (D15)
             __syncwarp();
+            if (m == K + 1) {   // the last merge: nothing reads sigma or D afterwards
+                if (act) alive &= ~(1u << bj);
+                break;
+            }
             if (act && l < 6) Sg[bi][l] = deq32(lobe[bi][1 + l]) / deq32(lobe[bi][0]);
             __syncwarp();
             float sn[4];
@@ -720,6 +726,7 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (lane < 7) list_[bi][lane] += list_[bj][lane];   // exact moment merge (D15)
             alive &= ~(1ull << bj);
             __syncwarp();
+            if (m == K + 1) break;   // the last merge: nothing reads sigma or D afterwards
             if (lane < 6) Sm[bi][lane] = deq32(list_[bi][1 + lane]) / deq32(list_[bi][0]);
             __syncwarp();
             {
@@ -878,6 +885,7 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (act && l < 7) H.lobe[bi][l] += H.lobe[bj][l];   // exact moment merge (D15)
             if (act) alive &= ~(1u << bj);
             __syncwarp();
+            if (m == K + 1) break;   // the last merge: nothing reads sigma or D afterwards
             if (act && l < 6) H.S[bi][l] = deq32(H.lobe[bi][1 + l]) / deq32(H.lobe[bi][0]);
             __syncwarp();
             if (act) {
