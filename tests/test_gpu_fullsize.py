@@ -69,3 +69,18 @@ def test_config3_fullsize_windowed(P):
     v.build_lod(c["levels"])
     k0 = v.level(0)["key"].cpu().numpy().astype(np.uint64)
     _check(v, c, 7, _cells(k0, 7, 3, np.random.default_rng(1)))
+
+
+def test_config5_8192_windowed(P):
+    # the largest grid of BASELINE's sweep: 32^3 voxel bins (15 local key bits), 13 levels
+    c = gen.config(5, n_segments=4_000_000, grid_res=8192)
+    v = P.Vox(c["grid_res"], c["bbox"])
+    v.voxelize_fibers(torch.from_numpy(c["segments"]).cuda(), torch.from_numpy(c["radii"]).cuda())
+    v.build_lod(c["levels"])
+    L0 = v.level(0)
+    k0 = L0["key"].cpu().numpy().astype(np.uint64)
+    tot = L0["acc"].sum(0)
+    del L0
+    for l in (1, 5, 9, c["levels"]):
+        assert torch.equal(v.level(l)["acc"].sum(0), tot)
+    _check(v, c, 5, _cells(k0, 5, 3, np.random.default_rng(2)))
