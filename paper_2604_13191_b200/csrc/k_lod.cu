@@ -1011,6 +1011,14 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
                                                          P.acc, P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
     }
     timer_end(c, c->t_prep);
+    // key, mass and m6 of the level are final here (SGGX-H only writes lobes): an event lets
+    // vox_copy_level_async start their D2H while the clustering runs
+    {
+        const int l = (int)(&P - c->lv);
+        if (!c->ev_level[l]) CK(cudaEventCreateWithFlags(&c->ev_level[l], cudaEventDisableTiming));
+        CK(cudaEventRecord(c->ev_level[l], c->stream));
+        c->ev_level_ok[l] = true;
+    }
     k_bucket_init<<<1, 32, 0, c->stream>>>(hist, K, MAXN, cursor, counts, c->d_lodwork);
     const uint64_t sb = (V + 256ull * SCATTER_PER_THREAD - 1) / (256ull * SCATTER_PER_THREAD);
     k_bucket_scatter<<<(unsigned)(sb ? sb : 1), 256, 0, c->stream>>>(nlob, V, K, MAXN, cursor, list);
@@ -1065,6 +1073,7 @@ vox_status build_level(vox_ctx* c, int l) {
     Level& C = c->lv[l - 1];
     Level& P = c->lv[l];
     free_level(c, P);
+    c->ev_level_ok[l] = false;
     const uint64_t n = C.n;
     const uint32_t K = c->K;
     if (n == 0) return VOX_OK;

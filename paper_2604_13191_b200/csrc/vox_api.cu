@@ -760,14 +760,24 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
     const uint64_t n = L.n;
     if (n == 0) return VOX_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    // key / mass / m6 are final once the level's prep ran (event recorded by the build), the
+    // lobes once everything enqueued so far has run
+    if (c->ev_level_ok[level]) CKS(cudaStreamWaitEvent(s, c->ev_level[level], 0));
+    else if (key || mass || m6) {
+        cudaEvent_t e0;
+        CKS(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+        CKS(cudaEventRecord(e0, c->stream));
+        CKS(cudaStreamWaitEvent(s, e0, 0));
+        CKS(cudaEventDestroy(e0));
+    }
+    if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, s));
+    if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, s));
+    if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, s));
     cudaEvent_t ev;
     CKS(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CKS(cudaEventRecord(ev, c->stream));      // after everything that produced the level
     CKS(cudaStreamWaitEvent(s, ev, 0));
     CKS(cudaEventDestroy(ev));
-    if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, s));
-    if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, s));
-    if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, s));
     if (ncl) CKS(cudaMemcpyAsync(ncl, L.ncl, n, cudaMemcpyDefault, s));
     if (cl) CKS(cudaMemcpyAsync(cl, L.cl, n * c->K * 28, cudaMemcpyDefault, s));
     return VOX_OK;
@@ -805,6 +815,7 @@ vox_status vox_import_level(vox_ctx* c, uint32_t level, const void* buf, uint64_
     vox_status s = ensure_dev(c);
     if (s != VOX_OK) return s;
     for (int l = (int)level + 1; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
+    for (int l = (int)level; l < VOX_MAX_LEVELS; l++) c->ev_level_ok[l] = false;   // arrays replaced
     s = unpack_level(c, (int)level, buf, bytes / rb);
     if (s != VOX_OK) return s;
     c->imported_level = (int)level;
@@ -896,6 +907,8 @@ void vox_destroy(vox_ctx* c) {
     ssync(c);
     release_mapped(c);
     density_reset(c);
+    for (int l = 0; l < VOX_MAX_LEVELS; l++)
+        if (c->ev_level[l]) cudaEventDestroy(c->ev_level[l]);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
                           &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode, &c->t_density}) {

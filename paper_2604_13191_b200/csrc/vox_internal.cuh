@@ -174,6 +174,8 @@ struct vox_ctx {
     std::string err;
     unsigned long long* dmask[VOX_MAX_LEVELS] = {};   // §13 sub-voxel masks per level ([n][8]), lazily
     int dmask_levels = -1;                  // levels with valid masks (0 after vox_density_*)
+    cudaEvent_t ev_level[VOX_MAX_LEVELS] = {};   // recorded when a level's key/mass/m6 are final
+    bool ev_level_ok[VOX_MAX_LEVELS] = {};
     void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
     void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
