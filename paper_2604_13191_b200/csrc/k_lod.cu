@@ -77,7 +77,6 @@ __global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* _
             else
                 for (int q = 0; q < cncl[x]; q++) n += cclacc[((uint64_t)x * K + q) * 7] != 0;
         }
-        pkey[p] = ckey[c0] >> 3;
 #pragma unroll
         for (int e = 0; e < 7; e++) pacc[7 * p + e] = sum[e];
         pmass[p] = deq32(sum[0]);
@@ -205,11 +204,9 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
         const int np = (int)(pe - p0);
         const uint32_t cs = start[p0];
         int c0 = 0, c1 = 0;
-        uint64_t k0 = 0;
         if (lane < np) {
             c0 = (int)(start[p0 + lane] - cs);
             c1 = (int)(start[p0 + lane + 1] - cs);
-            k0 = ckey[cs + c0];
         }
         mbar_wait(&s_bar[wib][b], (phase >> b) & 1u);
         phase ^= 1u << b;
@@ -224,7 +221,6 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
                 for (int e = 0; e < 7; e++) sum[e] += rows[7 * x + e];
                 n += rows[7 * x] > 0;
             }
-            pkey[p] = k0 >> 3;
 #pragma unroll
             for (int e = 0; e < 7; e++) sacc[7 * lane + e] = sum[e];
             nlob[p] = (uint8_t)n;
@@ -936,10 +932,15 @@ __global__ void k_pheads(const uint64_t* __restrict__ keys, uint64_t n, uint32_t
         flags[i] = (i == 0 || (keys[i] >> 3) != (keys[i - 1] >> 3)) ? 1u : 0u;
 }
 
+// parent run starts, and the parent keys (key of the run's first child >> 3)
 __global__ void k_pstarts(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ incl, uint64_t n,
-                          uint32_t* __restrict__ start) {
+                          uint32_t* __restrict__ start, const uint64_t* __restrict__ ckey,
+                          uint64_t* __restrict__ pkey) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (flags[i]) start[incl[i] - 1] = (uint32_t)i;
+        if (flags[i]) {
+            start[incl[i] - 1] = (uint32_t)i;
+            pkey[incl[i] - 1] = ckey[i] >> 3;
+        }
         if (i == n - 1) start[incl[i]] = (uint32_t)n;
     }
 }
@@ -1092,14 +1093,14 @@ vox_status build_level(vox_ctx* c, int l) {
     uint32_t V = 0;
     CK(readback(c, {{&V, incl + n - 1, 4}}));
     CK(dalloc(c, (void**)&start, ((uint64_t)V + 1) * 4));
-    k_pstarts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
+    CK(dalloc(c, (void**)&P.key, (uint64_t)V * 8));
+    k_pstarts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start, C.key, P.key);
     c->st.launches++;
     dfree(c, tmp);
     dfree(c, incl);
     dfree(c, flags);
     timer_end(c, c->t_lodscan);
     P.n = V;
-    CK(dalloc(c, (void**)&P.key, (uint64_t)V * 8));
     CK(dalloc(c, (void**)&P.acc, (uint64_t)V * 56));
     CK(dalloc(c, (void**)&P.mass, (uint64_t)V * 4));
     CK(dalloc(c, (void**)&P.m6, (uint64_t)V * 24));
