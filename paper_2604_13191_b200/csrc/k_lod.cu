@@ -138,9 +138,13 @@ constexpr int PREP_WARP_WORDS = 2 * PREP_ROWW + PREP_PAR * 7 + 2;   // + acc sta
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
 }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      (unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src), "r"(bytes), "r"(b)
@@ -183,22 +187,38 @@ k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__
     const uint64_t stride = (uint64_t)gridDim.x * PREP_WARPS * PREP_PAR;
     uint64_t p0 = (blockIdx.x * (uint64_t)PREP_WARPS + wib) * PREP_PAR;
     // issue the bulk copy of block q0's children into buffer b; returns the word offset
-    auto issue = [&](uint64_t q0, int b) {
-        const uint64_t qe = q0 + PREP_PAR < V ? q0 + PREP_PAR : V;
-        const uint64_t w0 = 7 * (uint64_t)start[q0], w1 = 7 * (uint64_t)start[qe];
+    // issue the bulk copy of the block whose child range [s0, s1) is given into buffer b
+    auto issue = [&](uint64_t s0, uint64_t s1, int b) {
+        const uint64_t w0 = 7 * s0, w1 = 7 * s1;
         const uint64_t a0 = w0 & ~1ull;                      // 16-byte aligned start word
         const unsigned bytes = (unsigned)(((w1 - a0) * 8 + 15) & ~15ull);
-        if (bytes) bulk_g2s(wbase + (size_t)b * PREP_ROWW, cacc + a0, bytes, &s_bar[wib][b]);
-        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                              (unsigned)__cvta_generic_to_shared(&s_bar[wib][b])) : "memory");
+        if (bytes) {
+            mbar_arrive_tx(&s_bar[wib][b], bytes);
+            bulk_g2s(wbase + (size_t)b * PREP_ROWW, cacc + a0, bytes, &s_bar[wib][b]);
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&s_bar[wib][b])) : "memory");
+        }
     };
-    if (lane == 0 && p0 < V) issue(p0, 0);
+    // child ranges of a block: start[q0], start[min(q0 + PREP_PAR, V)] (lane 0 only)
+    auto range = [&](uint64_t q0, uint64_t& s0, uint64_t& s1) {
+        s0 = start[q0];
+        s1 = start[q0 + PREP_PAR < V ? q0 + PREP_PAR : V];
+    };
+    uint64_t ns0 = 0, ns1 = 0;   // the range of the block after the next (prefetched a step ahead)
+    if (lane == 0 && p0 < V) {
+        uint64_t s0, s1;
+        range(p0, s0, s1);
+        issue(s0, s1, 0);
+        if (p0 + stride < V) range(p0 + stride, ns0, ns1);
+    }
     unsigned phase = 0;   // bit b: parity of buffer b's next completion
     for (int it = 0; p0 < V; p0 += stride, it++) {
         const int b = it & 1;
         if (lane == 0 && p0 + stride < V) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(p0 + stride, b ^ 1);
+            issue(ns0, ns1, b ^ 1);
+            if (p0 + 2 * stride < V) range(p0 + 2 * stride, ns0, ns1);   // consumed next iteration
         }
         const uint64_t pe = p0 + PREP_PAR < V ? p0 + PREP_PAR : V;
         const int np = (int)(pe - p0);
