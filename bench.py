@@ -438,7 +438,8 @@ def main():
         if fib and not args.sampled:
             v.stats_reset()
             v.density_fibers(d_a, d_b)
-            dens = [v.density_level(l) for l in range(levels + 1)]
+            top = levels if world == 1 else min(levels, int(math.log2(N)) - int(v.stats()["top_depth"]))
+            dens = [v.density_level(l) for l in range(top + 1)]   # sharded: masks are per shard
             st = v.stats()
             line["density"] = {"ms": st["ms_density"], "leaf_voxels": V[0],
                                "sub_voxel_tests_per_leaf": 512,
