@@ -56,9 +56,9 @@ __device__ __forceinline__ int pair_t(int i, int j) { return j * (j - 1) / 2 + i
 // (their lobes are copied in child-slot order); the others are counted per n so that the
 // SGGX-H kernels get them grouped by n (uniform work per warp).
 template <int K>
-__global__ void k_lod_prep(const uint64_t* __restrict__ ckey, const long long* __restrict__ cacc,
+__global__ void k_lod_prep(const long long* __restrict__ cacc,
                            const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc, int leaf,
-                           const uint32_t* __restrict__ start, uint64_t V, uint64_t* __restrict__ pkey,
+                           const uint32_t* __restrict__ start, uint64_t V,
                            long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
                            uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
                            uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
@@ -164,8 +164,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 
 template <int K>
 __global__ void __launch_bounds__(PREP_WARPS * 32)
-k_lod_prep_leaf(const uint64_t* __restrict__ ckey, const long long* __restrict__ cacc,
-                const uint32_t* __restrict__ start, uint64_t V, uint64_t* __restrict__ pkey,
+k_lod_prep_leaf(const long long* __restrict__ cacc,
+                const uint32_t* __restrict__ start, uint64_t V,
                 long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
                 uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
                 uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
@@ -1024,11 +1024,11 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 3);
         const size_t psm = (size_t)PREP_WARPS * (PREP_WARP_WORDS + PREP_PAR * K * 7) * sizeof(long long);
         CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-        k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.key, C.acc, start, V, P.key, P.acc,
+        k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.acc, start, V, P.acc,
                                                                             P.mass, P.m6, P.ncl, P.clacc, P.cl,
                                                                             nlob, hist);
     } else {
-        k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.key, C.acc, C.ncl, C.clacc, leaf, start, V, P.key,
+        k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.acc, C.ncl, C.clacc, leaf, start, V,
                                                          P.acc, P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
     }
     timer_end(c, c->t_prep);
