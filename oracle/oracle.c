@@ -1235,11 +1235,14 @@ int orc_sggxh_hist(int n, const int64_t* acc, int K, int N, int64_t* out) {
 static void jacobi3(const float S[6], float lam[3]) {
     float a[3][3] = {{S[0], S[3], S[4]}, {S[3], S[1], S[5]}, {S[4], S[5], S[2]}};
     static const int PQ[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-    for (int sweep = 0; sweep < 6; sweep++)
+    for (int sweep = 0; sweep < 6; sweep++) {
+        int rotated = 0;
         for (int m = 0; m < 3; m++) {
             int p = PQ[m][0], q = PQ[m][1], r = 3 - p - q;
             float apq = a[p][q];
-            if (apq == 0.0f) continue;
+            /* negligible off-diagonal (relative 2^-24 of the diagonal): no rotation */
+            if (!(fabsf(apq) * 16777216.0f > fabsf(a[p][p]) + fabsf(a[q][q]))) continue;
+            rotated = 1;
             float th = (a[q][q] - a[p][p]) / (2.0f * apq);
             float t = 1.0f / (fabsf(th) + sqrtf(th * th + 1.0f));
             if (th < 0.0f) t = -t;
@@ -1252,6 +1255,8 @@ static void jacobi3(const float S[6], float lam[3]) {
             a[r][p] = a[p][r] = c * arp - sn * arq;
             a[r][q] = a[q][r] = sn * arp + c * arq;
         }
+        if (!rotated) break;   /* a sweep without rotation: converged */
+    }
     lam[0] = a[0][0];
     lam[1] = a[1][1];
     lam[2] = a[2][2];

@@ -16,8 +16,9 @@ __device__ __forceinline__ void jacobi3(const float S[6], float lam[3]) {
     float a00 = S[0], a11 = S[1], a22 = S[2], a01 = S[3], a02 = S[4], a12 = S[5];
     // one rotation on (p, q) with r the third index; written out per pair so that every
     // matrix entry stays in a register
-    auto rot = [](float& app, float& aqq, float& apq, float& arp, float& arq) {
-        if (apq == 0.0f) return;
+    auto rot = [](float& app, float& aqq, float& apq, float& arp, float& arq) -> int {
+        // negligible off-diagonal (relative 2^-24 of the diagonal): no rotation
+        if (!(fabsf(apq) * 16777216.0f > fabsf(app) + fabsf(aqq))) return 0;
         const float th = (aqq - app) / (2.0f * apq);
         float t = 1.0f / (fabsf(th) + sqrtf(th * th + 1.0f));
         if (th < 0.0f) t = -t;
@@ -29,12 +30,13 @@ __device__ __forceinline__ void jacobi3(const float S[6], float lam[3]) {
         const float rp = arp, rq = arq;
         arp = c * rp - sn * rq;
         arq = sn * rp + c * rq;
+        return 1;
     };
     for (int sweep = 0; sweep < 6; sweep++) {
-        if (a01 == 0.0f && a02 == 0.0f && a12 == 0.0f) break;   // every further rotation is skipped
-        rot(a00, a11, a01, a02, a12);   // (0,1), r = 2: a_r0 = a02, a_r1 = a12
-        rot(a00, a22, a02, a01, a12);   // (0,2), r = 1: a_r0 = a01, a_r2 = a12
-        rot(a11, a22, a12, a01, a02);   // (1,2), r = 0: a_r1 = a01, a_r2 = a02
+        int rotated = rot(a00, a11, a01, a02, a12);   // (0,1), r = 2: a_r0 = a02, a_r1 = a12
+        rotated |= rot(a00, a22, a02, a01, a12);      // (0,2), r = 1: a_r0 = a01, a_r2 = a12
+        rotated |= rot(a11, a22, a12, a01, a02);      // (1,2), r = 0: a_r1 = a01, a_r2 = a02
+        if (!rotated) break;                          // a sweep without rotation: converged
     }
     lam[0] = a00;
     lam[1] = a11;
