@@ -433,7 +433,7 @@ def main():
                                                     for l in range(1, levels + 1))
         line["finalize"] = {"ms": st["ms_encode"], "records": recs, "records_per_s": recs / (st["ms_encode"] / 1e3),
                             "alg_bytes": byts, "achieved_gbs": byts / (st["ms_encode"] / 1e3) / 1e9,
-                            "bound": "alu (pinned Jacobi: ~18 rotations with IEEE div/sqrt per record)"}
+                            "bound": "alu (pinned Jacobi, 2-3 sweeps of IEEE div/sqrt rotations per record)"}
         # NEXT-2: sub-voxel occupancy and axis densities of every level (same ctx, after the build)
         if fib and not args.sampled:
             v.stats_reset()

@@ -947,24 +947,6 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     }
 }
 
-__global__ void k_pheads(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ flags) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        flags[i] = (i == 0 || (keys[i] >> 3) != (keys[i - 1] >> 3)) ? 1u : 0u;
-}
-
-// parent run starts, and the parent keys (key of the run's first child >> 3)
-__global__ void k_pstarts(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ incl, uint64_t n,
-                          uint32_t* __restrict__ start, const uint64_t* __restrict__ ckey,
-                          uint64_t* __restrict__ pkey) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (flags[i]) {
-            start[incl[i] - 1] = (uint32_t)i;
-            pkey[incl[i] - 1] = ckey[i] >> 3;
-        }
-        if (i == n - 1) start[incl[i]] = (uint32_t)n;
-    }
-}
-
 __global__ void k_finalize(uint64_t n, const long long* __restrict__ acc, float* __restrict__ mass,
                            float* __restrict__ m6, const uint8_t* __restrict__ ncl, const long long* __restrict__ clacc,
                            float* __restrict__ cl, int K) {
@@ -1090,6 +1072,62 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     return VOX_OK;
 }
 
+// Input iterator of the run-head flags of a sorted child key array (parent = key >> 3).
+struct HeadFlagIn {
+    const uint64_t* key;
+    int64_t base;
+    typedef std::random_access_iterator_tag iterator_category;
+    typedef uint32_t value_type;
+    typedef int64_t difference_type;
+    typedef const uint32_t* pointer;
+    typedef uint32_t reference;
+    __host__ __device__ uint32_t operator[](int64_t j) const {
+        const int64_t i = base + j;
+        return (i == 0 || (key[i] >> 3) != (key[i - 1] >> 3)) ? 1u : 0u;
+    }
+    __host__ __device__ uint32_t operator*() const { return (*this)[0]; }
+    __host__ __device__ HeadFlagIn operator+(int64_t d) const { return HeadFlagIn{key, base + d}; }
+};
+
+// Output "iterator" of that scan: position i receives the inclusive head count; a head writes
+// its parent's start (child index) and key; the last position closes start[] and the total.
+struct RunHeadOut {
+    const uint64_t* key;
+    uint32_t* start;
+    uint64_t* pkey;
+    uint64_t n;
+    uint32_t* total;
+    int64_t base;
+    struct Ref {
+        const uint64_t* key;
+        uint32_t* start;
+        uint64_t* pkey;
+        uint64_t n;
+        uint32_t* total;
+        int64_t i;
+        __device__ const Ref& operator=(uint32_t incl) const {
+            const uint64_t k = key[i];
+            if (i == 0 || (k >> 3) != (key[i - 1] >> 3)) {
+                start[incl - 1] = (uint32_t)i;
+                pkey[incl - 1] = k >> 3;
+            }
+            if ((uint64_t)i == n - 1) {
+                start[incl] = (uint32_t)n;
+                *total = incl;
+            }
+            return *this;
+        }
+    };
+    typedef std::random_access_iterator_tag iterator_category;
+    typedef uint32_t value_type;
+    typedef int64_t difference_type;
+    typedef void pointer;
+    typedef Ref reference;
+    __host__ __device__ Ref operator[](int64_t j) const { return Ref{key, start, pkey, n, total, base + j}; }
+    __host__ __device__ Ref operator*() const { return (*this)[0]; }
+    __host__ __device__ RunHeadOut operator+(int64_t d) const { return RunHeadOut{key, start, pkey, n, total, base + d}; }
+};
+
 vox_status build_level(vox_ctx* c, int l) {
     Level& C = c->lv[l - 1];
     Level& P = c->lv[l];
@@ -1099,26 +1137,26 @@ vox_status build_level(vox_ctx* c, int l) {
     const uint32_t K = c->K;
     if (n == 0) return VOX_OK;
     timer_begin(c, c->t_lodscan);
-    uint32_t *flags = nullptr, *incl = nullptr, *start = nullptr;
+    // one fused pass: run-head flags computed from the child keys on the fly (input iterator),
+    // their inclusive count scanned, and each head's parent start and key scattered by the
+    // output iterator -- no flag or count arrays. start / P.key are sized by n >= V.
+    uint32_t* start = nullptr;
+    uint32_t* total = nullptr;
     void* tmp = nullptr;
     size_t tb = 0;
-    CK(dalloc(c, (void**)&flags, n * 4));
-    CK(dalloc(c, (void**)&incl, n * 4));
-    k_pheads<<<grid_for(n), 256, 0, c->stream>>>(C.key, n, flags);
-    c->st.launches++;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flags, incl, (int64_t)n, c->stream));
+    CK(dalloc(c, (void**)&start, (n + 1) * 4));
+    CK(dalloc(c, (void**)&P.key, n * 8));
+    CK(dalloc(c, (void**)&total, 16));
+    HeadFlagIn in{C.key, 0};
+    RunHeadOut out{C.key, start, P.key, n, total, 0};
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int64_t)n, c->stream));
     CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
+    CK(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int64_t)n, c->stream));
     c->st.launches += 2;
     uint32_t V = 0;
-    CK(readback(c, {{&V, incl + n - 1, 4}}));
-    CK(dalloc(c, (void**)&start, ((uint64_t)V + 1) * 4));
-    CK(dalloc(c, (void**)&P.key, (uint64_t)V * 8));
-    k_pstarts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start, C.key, P.key);
-    c->st.launches++;
+    CK(readback(c, {{&V, total, 4}}));
     dfree(c, tmp);
-    dfree(c, incl);
-    dfree(c, flags);
+    dfree(c, total);
     timer_end(c, c->t_lodscan);
     P.n = V;
     CK(dalloc(c, (void**)&P.acc, (uint64_t)V * 56));
