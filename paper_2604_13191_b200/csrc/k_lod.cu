@@ -73,9 +73,12 @@ __global__ void k_lod_prep(const long long* __restrict__ cacc,
         for (uint32_t x = c0; x < c1; x++) {
 #pragma unroll
             for (int e = 0; e < 7; e++) sum[e] += cacc[7 * (uint64_t)x + e];
+            // stored lobes always have w > 0 (leaf lobes need mass > 0, merges add positives),
+            // so the dendrogram leaves are counted without reading them; should a w = 0 lobe
+            // ever appear, the copy below and the SGGX-H gathers still drop it (only the bucket
+            // choice would differ, not the result)
             if (leaf) n += cacc[7 * (uint64_t)x] > 0;
-            else
-                for (int q = 0; q < cncl[x]; q++) n += cclacc[((uint64_t)x * K + q) * 7] != 0;
+            else n += cncl[x];
         }
 #pragma unroll
         for (int e = 0; e < 7; e++) pacc[7 * p + e] = sum[e];
