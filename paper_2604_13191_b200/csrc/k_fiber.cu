@@ -260,6 +260,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t nbatch = (S + 31) / 32;
     const float PI_F = 3.14159274101257324f;   // 0x40490FDB
+    const bool whole = sh.cell_lo == 0 && sh.cell_hi == (1ull << (3 * g.logN - sh.shift));   // unsharded
     for (uint64_t batch = blockIdx.x * (uint64_t)EMIT_WARPS + wib; batch < nbatch;
          batch += (uint64_t)gridDim.x * EMIT_WARPS) {
         const uint64_t p = batch * 32 + lane;
@@ -273,7 +274,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             SegGeom G;
             seg_geom(g, s, rad[p], G);
             rg = G.rg;
-            if (!G.culled) {
+            if (!G.culled && (whole || box_in_shard(G.e0, G.e1, sh))) {
                 cnt = (uint32_t)((G.u1[0] - G.u0[0] + 1) * (G.u1[1] - G.u0[1] + 1) * (G.u1[2] - G.u0[2] + 1));
                 for (int ax = 0; ax < 3; ax++) s_u0[wib][ax][lane] = G.u0[ax];
                 s_ex[wib][0][lane] = (uint32_t)(G.u1[0] - G.u0[0] + 1);

@@ -209,8 +209,9 @@ struct TriSetup {
 };
 
 __global__ void k_tri_setup(const float* __restrict__ tri, const float* __restrict__ dirs, uint64_t T, GridXf gx,
-                            TriSetup* __restrict__ ts, unsigned long long* __restrict__ tcnt,
+                            Shard sh, TriSetup* __restrict__ ts, unsigned long long* __restrict__ tcnt,
                             float4* __restrict__ ptab) {
+    const bool whole = sh.cell_lo == 0 && sh.cell_hi == (1ull << (3 * gx.logN - sh.shift));   // unsharded
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
         float v[9];
         for (int q = 0; q < 9; q++) v[q] = tri[9 * t + q];
@@ -222,7 +223,7 @@ __global__ void k_tri_setup(const float* __restrict__ tri, const float* __restri
         TriSetup s;
         for (int q = 0; q < 9; q++) s.g[q] = G.g[q];
         unsigned long long cnt = 0;
-        if (!G.culled) {
+        if (!G.culled && (whole || box_in_shard(G.e0, G.e1, sh))) {   // no key in this shard: skipped
             for (int ax = 0; ax < 3; ax++) s.e0[ax] = (int)G.e0[ax];
             s.ex = (unsigned)(G.e1[0] - G.e0[0] + 1);
             s.ey = (unsigned)(G.e1[1] - G.e0[1] + 1);
@@ -321,7 +322,7 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
     if ((e = dalloc(c, (void**)&toff, (T + 1) * 8)) != cudaSuccess) return e;
     uint64_t blocks = (T + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
-    k_tri_setup<<<(unsigned)blocks, 256, 0, c->stream>>>(tri, dirs, T, c->g, ts, tcnt, ptab);
+    k_tri_setup<<<(unsigned)blocks, 256, 0, c->stream>>>(tri, dirs, T, c->g, sh, ts, tcnt, ptab);
     if ((e = cudaMemsetAsync(tcnt + T, 0, 8, c->stream)) != cudaSuccess) return e;
     if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt, toff, (int64_t)(T + 1), c->stream)) != cudaSuccess)
         return e;

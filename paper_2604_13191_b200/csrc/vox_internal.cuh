@@ -84,6 +84,22 @@ struct Shard {
     uint64_t cell_lo, cell_hi;
 };
 
+// Does the voxel box [e0, e1] (clamped to the grid) touch a top cell of the shard? Lets the
+// emit kernels skip primitives that have no key in this rank's Morton range (their keys would
+// all be filtered anyway), so per-rank emit work shrinks with the shard.
+__device__ __forceinline__ bool box_in_shard(const int64_t* e0, const int64_t* e1, const Shard& sh) {
+    const int s = sh.shift / 3;
+    const int64_t c0x = e0[0] >> s, c1x = e1[0] >> s, c0y = e0[1] >> s, c1y = e1[1] >> s;
+    const int64_t c0z = e0[2] >> s, c1z = e1[2] >> s;
+    for (int64_t cz = c0z; cz <= c1z; cz++)
+        for (int64_t cy = c0y; cy <= c1y; cy++)
+            for (int64_t cx = c0x; cx <= c1x; cx++) {
+                const uint64_t m = morton3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz);
+                if (m >= sh.cell_lo && m < sh.cell_hi) return true;
+            }
+    return false;
+}
+
 // Pair bins: Morton cells of 2^Lb voxels per edge (bin id = key >> shift, shift = 3 Lb).
 // Each bin owns the pair slots [off[b], off[b+1]) -- its exact candidate count, an upper
 // bound on its keys -- and cnt[b] pairs are appended there by the emit kernels.

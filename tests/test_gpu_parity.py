@@ -203,6 +203,25 @@ def test_fake_world_sharding_equals_unsharded(P):
                     assert torch.equal(g[key], ref[key]), (world, l, key)
 
 
+def test_fake_world_triangles(P):
+    """Sharded triangle voxelization (primitives outside a shard are skipped by its emit):
+    the union of the shards' local levels equals the unsharded result."""
+    c = gen.config(1)
+    T = torch.from_numpy(c["tris"]).cuda()
+    full = P.Vox(c["grid_res"], c["bbox"])
+    full.voxelize_triangles(T)
+    full.build_lod(c["levels"])
+    for world in (2, 5):
+        shards = [P.Vox(c["grid_res"], c["bbox"], rank=q, world=world) for q in range(world)]
+        for v in shards:
+            v.voxelize_triangles(T)
+            v.build_lod(c["levels"])
+        lt = shards[0].built_levels()
+        for l in range(lt + 1):
+            for key in ("key", "acc", "ncl", "cl"):
+                assert torch.equal(torch.cat([v.level(l)[key] for v in shards]), full.level(l)[key]), (world, l, key)
+
+
 def test_deterministic_repeat(P):
     c = gen.config(2)
     outs = []
