@@ -233,3 +233,36 @@ def test_deterministic_repeat(P):
     for a, b in zip(*outs):
         for k in a:
             assert torch.equal(a[k], b[k])
+
+
+def test_edge_cases_new_entry_points(P):
+    """Empty and degenerate inputs through the NEXT-row entry points: no-ops where nothing is
+    hit, exact agreement with the oracle where something is."""
+    bbox = np.array([0, 0, 0, 1, 1, 1], np.float32)
+    v = P.Vox(16, bbox)
+    # nothing inside the grid: every primitive outside the bbox
+    far = torch.tensor([[[5.0, 5.0, 5.0], [6.0, 6.0, 6.0]]], device="cuda")
+    v.voxelize_fibers(far, torch.tensor([0.1], device="cuda"))
+    v.sample_splines(torch.tensor([[[5.0, 5, 5], [6, 6, 6], [7, 7, 7], [8, 8, 8]]], device="cuda"),
+                     torch.tensor([0.1], device="cuda"), 4)
+    v.build_lod(4)
+    assert all(int(v.view(l)["n"]) == 0 for l in range(5))
+    assert v.encode_level(2)["sggx6"].numel() == 0
+    v.density_fibers(far, torch.tensor([0.1], device="cuda"))
+    assert v.density_level(3)["occ"].numel() == 0
+    # zero-area and zero-length primitives: keys without mass, zero samples
+    w = P.Vox(16, bbox)
+    o = oracle.Oracle(16, bbox)
+    tri = np.array([[[0.3, 0.3, 0.3], [0.3, 0.3, 0.3], [0.3, 0.3, 0.3]],
+                    [[0.1, 0.2, 0.5], [0.8, 0.3, 0.5], [0.4, 0.9, 0.5]]], np.float32)
+    w.sample_triangles(torch.from_numpy(tri).cuda(), None, 9)
+    o.sample_triangles(tri, None, 9)
+    seg = np.array([[[0.5, 0.5, 0.5], [0.5, 0.5, 0.5]]], np.float32)
+    w.voxelize_fibers(torch.from_numpy(seg).cuda(), torch.tensor([0.03], device="cuda"))
+    o.add_fibers(seg, np.array([0.03], np.float32))
+    w.build_lod(4)
+    o.build(4)
+    for l in range(5):
+        _cmp_level(w.level(l), o.level(l), l, "edge")
+    codes, _ = oracle.encode(o.level(0)["acc"])
+    assert np.array_equal(w.encode_level(0)["sggx6"].cpu().numpy(), codes)
