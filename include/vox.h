@@ -180,10 +180,12 @@ vox_status vox_density_level(vox_ctx* ctx, uint32_t level, float* occ, float* ax
 vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags);
 
 /* Like vox_copy_level but asynchronous on the caller's `stream` (a cudaStream_t, NULL = the
- * legacy default stream): the copies are ordered after the work already enqueued on the ctx
- * stream (an event), and the call returns without synchronising, so the D2H of level l
- * overlaps the build of levels > l. Building further levels does not touch lower levels;
- * the caller synchronises `stream` before reading the buffers or destroying the ctx.
+ * legacy default stream) and without synchronising: key / mass / m6 are ordered after the
+ * level's prep (they are final there; an event recorded by the build), ncl / cl after all
+ * work enqueued on the ctx stream so far (an event), so the D2H of level l overlaps the
+ * clustering of level l and the build of levels > l. Building further levels does not touch
+ * lower levels; the caller synchronises `stream` before reading the buffers or destroying
+ * the ctx.
  * Level 0 supports key / mass / m6 only (ncl or cl non-NULL -> VOX_ERR_INVALID_ARG). */
 vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                                 uint8_t* ncl, float* cl, void* stream);
