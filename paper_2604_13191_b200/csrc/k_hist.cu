@@ -149,16 +149,28 @@ __device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* c
         C[q] = 0;
         W[q] = 0;
     }
-#pragma unroll 2
-    for (int r = 0; r < HR; r++) {
-        const unsigned w = __ldg(pg + r * 32 + lane);   // (gap << 8) | cell, L1-resident
-        const int b = (int)(w & 0xffu);
-        const unsigned g = w >> 8;
-        const int hi = Hi[b];
+    static_assert(HR % 4 == 0, "slice steps in groups of four");
+    for (int r0 = 0; r0 < HR; r0 += 4) {
+        // four table words and their histogram reads issued before the dependent sums
+        unsigned w[4];
+        int hi[4], hj[4][R];
 #pragma unroll
-        for (int q = 0; q < R; q++) {
-            C[q] += hi - (int)Hj[q][b];
-            W[q] += (unsigned long long)(unsigned)(C[q] < 0 ? -C[q] : C[q]) * g;
+        for (int k = 0; k < 4; k++) w[k] = __ldg(pg + (r0 + k) * 32 + lane);   // (gap << 8) | cell
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int b = (int)(w[k] & 0xffu);
+            hi[k] = Hi[b];
+#pragma unroll
+            for (int q = 0; q < R; q++) hj[k][q] = Hj[q][b];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const unsigned g = w[k] >> 8;
+#pragma unroll
+            for (int q = 0; q < R; q++) {
+                C[q] += hi[k] - hj[k][q];
+                W[q] += (unsigned long long)(unsigned)(C[q] < 0 ? -C[q] : C[q]) * g;
+            }
         }
     }
 #pragma unroll
