@@ -57,6 +57,11 @@ typedef struct {
                             * histogram distance (§10: N samples per SGGX, 5x5x5 bins, sliced W1;
                             * P:383-389) */
     uint32_t hist_samples; /* N of distance_mode 1, 32..8160 (0 = 5000) */
+    uint64_t part_candidates; /* candidate voxels per Morton part of one voxelize call
+                               * (0 = 3*2^30, also the maximum): a call with more candidates
+                               * runs part by part over this rank's top-cell range, which
+                               * bounds its pair scratch (16 B per candidate); the result is
+                               * identical */
 } vox_options;
 
 /* Level view. Level 0 (leaves): ncl and cl are NULL; a leaf holds exactly one lobe

@@ -35,7 +35,8 @@ class VoxError(RuntimeError):
 class _Options(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("rank", C.c_int), ("world", C.c_int), ("top_depth", C.c_int),
                 ("k", C.c_uint32), ("n_slices", C.c_uint32), ("max_bytes", C.c_uint64), ("profile", C.c_int),
-                ("distance_mode", C.c_int), ("hist_samples", C.c_uint32)]
+                ("distance_mode", C.c_int), ("hist_samples", C.c_uint32),
+                ("part_candidates", C.c_uint64)]
 
 
 class _View(C.Structure):
@@ -168,7 +169,7 @@ class Vox:
 
     def __init__(self, grid_res: int, bbox, k: int = 3, rank: int = 0, world: int = 1, top_depth: int = 0,
                  max_bytes: int = 0, profile: bool = False, stream=None, distance: str = "sigma",
-                 hist_samples: int = 5000):
+                 hist_samples: int = 5000, part_candidates: int = 0):
         import torch
         self.grid_res = int(grid_res)
         self.k = int(k)
@@ -182,7 +183,8 @@ class Vox:
             raise ValueError(f"distance must be 'sigma' or 'hist', not {distance!r}")
         self.distance = distance
         opt = _Options(C.c_void_p(stream.cuda_stream), int(rank), int(world), int(top_depth), int(k), 32,
-                       int(max_bytes), int(bool(profile)), 1 if distance == "hist" else 0, int(hist_samples))
+                       int(max_bytes), int(bool(profile)), 1 if distance == "hist" else 0, int(hist_samples),
+                       int(part_candidates))
         h = C.c_void_p()
         st = lib().vox_create(C.byref(h), self.grid_res, bb, C.byref(opt))
         if st:

@@ -92,9 +92,46 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     return VOX_OK;
 }
 
-static vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6,
-                                  uint64_t V) {
+vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6, uint64_t V) {
     Level& L0 = c->lv[0];
+    if (V == 0) {
+        dfree(c, nkey);
+        dfree(c, nacc);
+        dfree(c, nmass);
+        dfree(c, nm6);
+        return VOX_OK;
+    }
+    if (L0.n > 0) {
+        // disjoint, ordered key ranges (the Morton parts of one call): concatenation
+        uint64_t last = 0, first = 0;
+        CK(readback(c, {{&last, L0.key + L0.n - 1, 8}, {&first, nkey, 8}}));
+        if (first > last) {
+            timer_begin(c, c->t_merge);
+            const uint64_t tot = L0.n + V;
+            Level M;
+            M.n = tot;
+            CK(dalloc(c, (void**)&M.key, tot * 8));
+            CK(dalloc(c, (void**)&M.acc, tot * 56));
+            CK(dalloc(c, (void**)&M.mass, tot * 4));
+            CK(dalloc(c, (void**)&M.m6, tot * 24));
+            CK(cudaMemcpyAsync(M.key, L0.key, L0.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.key + L0.n, nkey, V * 8, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.acc, L0.acc, L0.n * 56, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.acc + 7 * L0.n, nacc, V * 56, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.mass, L0.mass, L0.n * 4, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.mass + L0.n, nmass, V * 4, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.m6, L0.m6, L0.n * 24, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(M.m6 + 6 * L0.n, nm6, V * 24, cudaMemcpyDeviceToDevice, c->stream));
+            dfree(c, nkey);
+            dfree(c, nacc);
+            dfree(c, nmass);
+            dfree(c, nm6);
+            free_level(c, L0);
+            L0 = M;
+            timer_end(c, c->t_merge);
+            return VOX_OK;
+        }
+    }
     if (L0.n == 0) {
         free_level(c, L0);
         L0.n = V;
@@ -546,7 +583,7 @@ vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigne
 }
 
 vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, Bins bins, uint64_t nb,
-                       const float4* ptab) {
+                       const float4* ptab, LeafSet& out) {
     const int lbits = bins.shift;
     const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
     unsigned* vcount = nullptr;
@@ -575,7 +612,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     unsigned long long P = 0;
     CK(readback(c, {{&V, voff + nb, 4}, {&P, npairs, 8}}));
     timer_end(c, c->t_sort);
-    c->st.pairs = P;
+    c->st.pairs += P;
     timer_begin(c, c->t_reduce);
     uint64_t* nkey = nullptr;
     long long* nacc = nullptr;
@@ -608,8 +645,12 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     dfree(c, npairs);
     dfree(c, alist);
     dfree(c, big);
-    c->st.voxels = V;
-    return merge_into_leaf(c, nkey, nacc, nmass, nm6, V);
+    out.key = nkey;
+    out.acc = nacc;
+    out.mass = nmass;
+    out.m6 = nm6;
+    out.n = V;
+    return VOX_OK;
 }
 
 }  // namespace vox

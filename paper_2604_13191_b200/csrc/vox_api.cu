@@ -56,9 +56,15 @@ cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
     cudaError_t e = cudaSuccess;
     if (!*p) {
         e = cudaMallocAsync(p, want, c->stream);
-        if (e == cudaErrorMemoryAllocation) {   // release cached blocks of this stream and retry
+        if (e == cudaErrorMemoryAllocation) {
+            // release the cached blocks of this stream, return the pool's unused memory, retry
             cudaGetLastError();
             vox_trim_stream(c->stream);
+            cudaStreamSynchronize(c->stream);
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+                cudaMemPoolTrimTo(pool, 0);
             e = cudaMallocAsync(p, want, c->stream);
         }
         if (e == cudaSuccess) {
@@ -290,6 +296,8 @@ vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], con
     if (o.distance_mode < 0 || o.distance_mode > 1) return VOX_ERR_INVALID_ARG;
     if (o.hist_samples == 0) o.hist_samples = 5000;
     if (o.hist_samples < 32 || o.hist_samples > 8160) return VOX_ERR_INVALID_ARG;
+    if (o.part_candidates == 0) o.part_candidates = 3ull << 30;
+    if (o.part_candidates > (3ull << 30)) return VOX_ERR_INVALID_ARG;
     vox_ctx* c = new (std::nothrow) vox_ctx();
     if (!c) return VOX_ERR_OOM;
     for (int a = 0; a < 3; a++) c->g.bmin[a] = bbox[a];
@@ -306,6 +314,7 @@ vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], con
     c->profile = o.profile;
     c->dmode = o.distance_mode;
     c->hist_n = (int)o.hist_samples;
+    c->part_cand = o.part_candidates;
     c->built = 0;
     c->st.top_depth = (uint32_t)c->T;
     *out = c;
@@ -380,61 +389,120 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
         c->st.cell_lo = c->cell_lo;
         c->st.cell_hi = c->cell_hi;
     }
-    unsigned long long* off = nullptr;
-    uint64_t cap = 0;
-    s = bin_offsets(c, Wb, Lb, &off, &cap);
-    dfree(c, Wb);
-    if (s != VOX_OK) return s;
-    c->st.candidates = cap;
+    // Parts: this rank's top-cell range, split (in Morton order) so that every part's candidate
+    // count fits the 32-bit pair slots (and the part_candidates bound). Each part emits only its
+    // keys (the shard filter; a primitive's S_p still sums all its keys) and its leaves follow
+    // the previous part's in key order, so the parts' leaf sets are concatenated.
+    const uint64_t lo0 = c->cell_lo, hi0 = c->cell_hi;
+    std::vector<uint64_t> cuts = {lo0, hi0};
+    {
+        unsigned long long* off = nullptr;
+        uint64_t cap = 0;
+        s = bin_offsets(c, Wb, Lb, &off, &cap);
+        if (s != VOX_OK) { dfree(c, Wb); return s; }
+        dfree(c, off);
+        c->st.candidates = cap;
+        if (cap > c->part_cand) {
+            std::vector<uint64_t> W;
+            s = bin_topcells(c, Wb, Lb, W);
+            if (s != VOX_OK) { dfree(c, Wb); return s; }
+            cuts = {lo0};
+            uint64_t acc = 0;
+            for (uint64_t x = lo0; x < hi0; x++) {
+                if (W[x] >= (3ull << 30)) {   // one top cell must fit the 32-bit pair slots
+                    dfree(c, Wb);
+                    c->err = "a top cell with more than 3*2^30 candidate voxels: use a larger top_depth";
+                    return VOX_ERR_CAPACITY;
+                }
+                if (acc > 0 && acc + W[x] > c->part_cand) {
+                    cuts.push_back(x);
+                    acc = 0;
+                }
+                acc += W[x];
+            }
+            cuts.push_back(hi0);
+        }
+    }
     c->st.pairs = 0;
-    if (cap >= (1ull << 32)) {
-        dfree(c, off);
-        c->err = "more than 2^32 candidate voxels in one call: split the primitives into batches";
-        return VOX_ERR_CAPACITY;
+    auto run_part = [&]() -> vox_status {
+        unsigned long long* off = nullptr;
+        uint64_t cap = 0;
+        vox_status r = bin_offsets(c, Wb, Lb, &off, &cap);
+        if (r != VOX_OK) return r;
+        if (cap == 0) {
+            dfree(c, off);
+            return VOX_OK;
+        }
+        // estimate: pairs + per-bin scans + new leaf (<= cap voxels) + prim table + merge
+        const uint64_t est = cap * 16 + nb * 24 + cap * 92 + nptab * 16 + c->lv[0].n * 92;
+        if (c->max_bytes && est > c->max_bytes) {
+            dfree(c, off);
+            c->err = "estimated " + std::to_string(est) + " bytes exceed max_bytes";
+            return VOX_ERR_CAPACITY;
+        }
+        uint64_t *keys = nullptr, *vals = nullptr;
+        float4* ptab = nullptr;
+        unsigned* bcnt = nullptr;
+        auto release = [&]() {   // pair scratch, released before the leaf merge
+            dfree(c, keys);
+            dfree(c, vals);
+            dfree(c, ptab);
+            dfree(c, bcnt);
+            dfree(c, off);
+        };
+        cudaError_t e = dalloc(c, (void**)&keys, cap * 8);
+        if (e == cudaSuccess) e = dalloc(c, (void**)&vals, cap * 8);
+        if (e == cudaSuccess) e = dalloc(c, (void**)&ptab, nptab * sizeof(float4));
+        if (e == cudaSuccess) e = dalloc(c, (void**)&bcnt, nb * 4);
+        if (e == cudaSuccess) e = cudaMemsetAsync(bcnt, 0, nb * 4, c->stream);
+        if (e != cudaSuccess) {
+            release();
+            c->err = std::string("voxelize scratch: ") + cudaGetErrorString(e);
+            return e == cudaErrorMemoryAllocation ? VOX_ERR_OOM : VOX_ERR_CUDA;
+        }
+        Shard sh;
+        sh.shift = 3 * (c->g.logN - c->T);
+        sh.cell_lo = c->cell_lo;
+        sh.cell_hi = c->cell_hi;
+        Bins bins;
+        bins.shift = 3 * Lb;
+        bins.off = off;
+        bins.cnt = bcnt;
+        timer_begin(c, c->t_emit);
+        e = emit(c, a, b, n, sh, bins, keys, vals, ptab);
+        timer_end(c, c->t_emit);
+        if (e != cudaSuccess) {
+            release();
+            c->err = std::string("emit: ") + cudaGetErrorString(e);
+            return VOX_ERR_CUDA;
+        }
+        LeafSet leaf;
+        r = reduce_bins(c, keys, vals, bins, nb, ptab, leaf);
+        unsigned fl2 = 0;
+        e = r == VOX_OK ? readback(c, {{&fl2, c->d_flags, 4}}) : cudaSuccess;
+        release();
+        if (r != VOX_OK) return r;
+        if (e != cudaSuccess) {
+            c->err = std::string("readback: ") + cudaGetErrorString(e);
+            return e == cudaErrorMemoryAllocation ? VOX_ERR_OOM : VOX_ERR_CUDA;
+        }
+        if (fl2 & VOX_EFLAG_OVERFLOW) {
+            c->err = "internal: pair capacity overflow";
+            return VOX_ERR_CUDA;
+        }
+        return merge_into_leaf(c, leaf.key, leaf.acc, leaf.mass, leaf.m6, leaf.n);
+    };
+    vox_status res = VOX_OK;
+    for (size_t part = 0; part + 1 < cuts.size() && res == VOX_OK; part++) {
+        c->cell_lo = cuts[part];
+        c->cell_hi = cuts[part + 1];
+        res = run_part();
     }
-    if (cap == 0) {
-        dfree(c, off);
-        c->state = ST_VOXELIZED;
-        return VOX_OK;
-    }
-    // estimate: pairs + per-bin scans + new leaf (<= cap voxels) + prim table + merge
-    const uint64_t est = cap * 16 + nb * 24 + cap * 92 + nptab * 16 + c->lv[0].n * 92;
-    if (c->max_bytes && est > c->max_bytes) {
-        dfree(c, off);
-        c->err = "estimated " + std::to_string(est) + " bytes exceed max_bytes";
-        return VOX_ERR_CAPACITY;
-    }
-    uint64_t *keys = nullptr, *vals = nullptr;
-    float4* ptab = nullptr;
-    unsigned* bcnt = nullptr;
-    CKS(dalloc(c, (void**)&keys, cap * 8));
-    CKS(dalloc(c, (void**)&vals, cap * 8));
-    CKS(dalloc(c, (void**)&ptab, nptab * sizeof(float4)));
-    CKS(dalloc(c, (void**)&bcnt, nb * 4));
-    CKS(cudaMemsetAsync(bcnt, 0, nb * 4, c->stream));
-    Shard sh;
-    sh.shift = 3 * (c->g.logN - c->T);
-    sh.cell_lo = c->cell_lo;
-    sh.cell_hi = c->cell_hi;
-    Bins bins;
-    bins.shift = 3 * Lb;
-    bins.off = off;
-    bins.cnt = bcnt;
-    timer_begin(c, c->t_emit);
-    CKS(emit(c, a, b, n, sh, bins, keys, vals, ptab));
-    timer_end(c, c->t_emit);
-    s = reduce_bins(c, keys, vals, bins, nb, ptab);
-    CKS(readback(c, {{&fl, c->d_flags, 4}}));
-    dfree(c, keys);
-    dfree(c, vals);
-    dfree(c, ptab);
-    dfree(c, bcnt);
-    dfree(c, off);
-    if (s != VOX_OK) return s;
-    if (fl & VOX_EFLAG_OVERFLOW) {
-        c->err = "internal: pair capacity overflow";
-        return VOX_ERR_CUDA;
-    }
+    c->cell_lo = lo0;
+    c->cell_hi = hi0;
+    dfree(c, Wb);
+    if (res != VOX_OK) return res;
+    c->st.voxels = c->lv[0].n;
     c->state = ST_VOXELIZED;
     return VOX_OK;
 }

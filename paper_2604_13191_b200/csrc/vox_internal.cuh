@@ -175,6 +175,7 @@ struct vox_ctx {
     int rank = 0, world = 1, T = 0;
     uint32_t K = 3;
     uint64_t max_bytes = 0;
+    uint64_t part_cand = 3ull << 30;   // candidates per Morton part of one voxelize call
     int profile = 0;
     int state = vox::ST_CREATED;
     int built = 0;
@@ -235,8 +236,17 @@ cudaError_t launch_tri_bound(vox_ctx* c, const float* tri, const float* dirs, ui
 cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uint64_t T, Shard sh, Bins bins,
                             uint64_t* keys, uint64_t* vals, float4* ptab);
 // binned reduce (k_reduce.cu): per-bin pair lists -> new leaf set merged into lv[0]
+struct LeafSet {
+    uint64_t* key = nullptr;
+    long long* acc = nullptr;
+    float* mass = nullptr;
+    float* m6 = nullptr;
+    uint64_t n = 0;
+};
 vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, Bins bins, uint64_t nb,
-                       const float4* ptab);
+                       const float4* ptab, LeafSet& out);
+// merges a new leaf set into lv[0] (concatenation when its keys follow, exact sums otherwise)
+vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6, uint64_t V);
 // per-call helpers (k_reduce.cu)
 vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT);
 vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigned long long** off_out,

@@ -108,6 +108,27 @@ def test_mixed_and_split_calls(P):
         _cmp_level(v.level(l), o.level(l), l, "mixed")
 
 
+@pytest.mark.parametrize("part", [1, 5000, 60000])
+def test_morton_parts_equal_one_pass(P, part):
+    """A call cut into Morton parts (part_candidates; the > 2^32-candidate path of config 5 at
+    8192^3) gives the oracle's result: fibers, then triangles accumulating into the same leaves,
+    with part = 1 forcing one part per non-empty top cell."""
+    s, r = gen.plain_weave(n_warp=16, n_weft=16, n_seg=32, pitch=1 / 16)
+    tris = gen.icosphere(2, radius=0.3)
+    v = P.Vox(128, [0, 0, 0, 1, 1, 1], part_candidates=part)
+    o = oracle.Oracle(128, np.array([0, 0, 0, 1, 1, 1], np.float32))
+    v.voxelize_fibers(torch.from_numpy(s).cuda(), torch.from_numpy(r).cuda())
+    st = v.stats()
+    assert st["candidates"] > part
+    v.voxelize_triangles(torch.from_numpy(tris).cuda())
+    o.add_fibers(s, r)
+    o.add_triangles(tris)
+    v.build_lod(7)
+    o.build(7)
+    for l in range(8):
+        _cmp_level(v.level(l), o.level(l), l, f"parts{part}")
+
+
 def test_host_entry_points(P):
     c = gen.config(1)
     v = P.Vox(c["grid_res"], c["bbox"])
