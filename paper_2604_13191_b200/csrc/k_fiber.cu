@@ -176,18 +176,22 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
 // every point of the box lies within sqrt(3)/2 of the centre and the pinned fp32 predicate
 // deviates from the exact one by orders of magnitude less than 0.05 voxel. Parity tests
 // compare the emitted key sets with the oracle, which has no such shortcut.
-__device__ __forceinline__ bool far_from_capsule(const Fib& f, const float* d, float rg, int64_t i, int64_t j,
-                                                 int64_t k) {
-    const float e0 = ((float)i + 0.5f) - f.a[0], e1 = ((float)j + 0.5f) - f.a[1], e2 = ((float)k + 0.5f) - f.a[2];
-    const float ww = f.w[0] + f.w[1] + f.w[2];
-    float t = 0.0f;
-    if (ww > 0.0f) {
-        t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) / ww;
-        t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
-    }
+__device__ __forceinline__ bool far_from_capsule(const float* a, const float* d, float iww, float thr2, int64_t i,
+                                                 int64_t j, int64_t k) {
+    const float e0 = ((float)i + 0.5f) - a[0], e1 = ((float)j + 0.5f) - a[1], e2 = ((float)k + 0.5f) - a[2];
+    float t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) * iww;   // iww = 1 / |d|^2 (0 for a sphere)
+    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
     const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
-    const float thr = rg + 0.91602540378f;   // sqrt(3)/2 + 0.05
-    return q0 * q0 + q1 * q1 + q2 * q2 > thr * thr;
+    return q0 * q0 + q1 * q1 + q2 * q2 > thr2;
+}
+// the per-segment constants of far_from_capsule: 1 / |d|^2 and (rg + sqrt(3)/2 + 0.05)^2. A
+// rounded t only moves the nearest point along the segment, which changes the distance by
+// O(|d| * 2^-24)^2 -- far inside the 0.05-voxel margin.
+__device__ __forceinline__ void far_consts(const float* w, float rg, float& iww, float& thr2) {
+    const float ww = w[0] + w[1] + w[2];
+    iww = ww > 0.0f ? 1.0f / ww : 0.0f;
+    const float thr = rg + 0.91602540378f;
+    thr2 = thr * thr;
 }
 
 // ---------------------------------------------------------------- emit
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 3)
 k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g, Shard sh,
              Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab,
              unsigned* __restrict__ flags) {
-    __shared__ float s_f[EMIT_WARPS][16][32];
+    __shared__ float s_f[EMIT_WARPS][18][32];
     __shared__ int64_t s_u0[EMIT_WARPS][3][32];
     __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
     __shared__ uint32_t s_start[EMIT_WARPS][32];
@@ -302,6 +306,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             s_f[wib][11][lane] = f.len;
             for (int ax = 0; ax < 3; ax++) s_f[wib][12 + ax][lane] = d[ax];
             s_f[wib][15][lane] = rg;
+            far_consts(f.w, rg, s_f[wib][16][lane], s_f[wib][17][lane]);
         }
         // warp inclusive scan of the candidate counts
         uint32_t incl = cnt;
@@ -332,14 +337,12 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                 const int64_t i = s_u0[wib][0][o] + (int64_t)(local - t * ex);
                 const int64_t j = s_u0[wib][1][o] + (int64_t)(t % ey);
                 const int64_t k = s_u0[wib][2][o] + (int64_t)(t / ey);
-                Fib fo;
-                float dv[3];
+                float av[3], dv[3];
                 for (int ax = 0; ax < 3; ax++) {
-                    fo.a[ax] = s_f[wib][ax][o];
-                    fo.w[ax] = s_f[wib][3 + ax][o];
+                    av[ax] = s_f[wib][ax][o];
                     dv[ax] = s_f[wib][12 + ax][o];
                 }
-                surv = !far_from_capsule(fo, dv, s_f[wib][15][o], i, j, k);
+                surv = !far_from_capsule(av, dv, s_f[wib][16][o], s_f[wib][17][o], i, j, k);
                 ent = make_int4(o, (int)i, (int)j, (int)k);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, surv);
@@ -414,15 +417,11 @@ __device__ __forceinline__ void fib_setup(Fib& f, float (&d)[3], const float* a,
 // centre distance^2 of fine voxel (x,y,z) to the segment, and (box2) the squared distance from
 // the segment point nearest the centre to the box (GPU-only shortcut geometry: the
 // segment-box distance lies in [sqrt(c2) - sqrt(3)/2, sqrt(box2)])
-__device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, int64_t x, int64_t y, int64_t z,
+__device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, float iww, int64_t x, int64_t y, int64_t z,
                                               float& box2) {
     const float e0 = ((float)x + 0.5f) - f.a[0], e1 = ((float)y + 0.5f) - f.a[1], e2 = ((float)z + 0.5f) - f.a[2];
-    const float ww = f.w[0] + f.w[1] + f.w[2];
-    float t = 0.0f;
-    if (ww > 0.0f) {
-        t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) / ww;
-        t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
-    }
+    float t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) * iww;   // iww = 1 / |d|^2 (0 for a sphere)
+    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
     const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
     const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f), o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
     box2 = o0 * o0 + o1 * o1 + o2 * o2;
@@ -458,6 +457,9 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
         }
         const float rg8 = 8.0f * G.rg;
         fib_setup(f8, d8, a8, b8, rg8);
+        float iww, thr2, iww8, unused;
+        far_consts(f.w, G.rg, iww, thr2);
+        far_consts(f8.w, rg8, iww8, unused);
         // the centre is in the box: dist(segment, box) <= dist(segment, centre) and >= it - sqrt(3)/2
         const float far = rg8 + 1.11602540378f, near = rg8 - 0.25f;   // margins 0.25 fine voxel
         const float far2 = far * far, near2 = near > 0.0f ? near * near : -1.0f;
@@ -472,18 +474,17 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                 j = G.e0[1] + (cidx / ex) % ey;
                 k = G.e0[2] + cidx / (ex * ey);
                 float ell;
-                key = !far_from_capsule(f, d, G.rg, i, j, k) && fiber_key(f, i, j, k, ell);
+                key = !far_from_capsule(f.a, d, iww, thr2, i, j, k) && fiber_key(f, i, j, k, ell);
             }
-            unsigned bal = __ballot_sync(0xffffffffu, key);
+            // every key lane searches its leaf at once (the searches' load latencies overlap)
+            const long long my_idx = key ? find_key(keys0, n0, morton3((uint32_t)i, (uint32_t)j, (uint32_t)k)) : -1;
+            unsigned bal = __ballot_sync(0xffffffffu, my_idx >= 0);
             while (bal) {
                 const int src = __ffs(bal) - 1;
                 bal &= bal - 1;
                 const int64_t vi = __shfl_sync(0xffffffffu, i, src), vj = __shfl_sync(0xffffffffu, j, src),
                               vk = __shfl_sync(0xffffffffu, k, src);
-                long long idx = -1;
-                if (lane == 0) idx = find_key(keys0, n0, morton3((uint32_t)vi, (uint32_t)vj, (uint32_t)vk));
-                idx = __shfl_sync(0xffffffffu, idx, 0);
-                if (idx < 0) continue;
+                const long long idx = __shfl_sync(0xffffffffu, my_idx, src);
                 // classify the 512 sub-voxels (16 per lane): sure hits straight into the mask,
                 // undecided ones queued, then the queue evaluated 32 at a time (no divergence)
                 int nq = 0;
@@ -492,7 +493,7 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                     const int sub = lane + 32 * q;
                     const int64_t x = 8 * vi + (sub & 7), y = 8 * vj + ((sub >> 3) & 7), z = 8 * vk + (sub >> 6);
                     float box2;
-                    const float c2 = centre_dist2(f8, d8, x, y, z, box2);
+                    const float c2 = centre_dist2(f8, d8, iww8, x, y, z, box2);
                     const bool sure = box2 < near2, open = !sure && !(c2 > far2);
                     const unsigned bs = __ballot_sync(0xffffffffu, sure);
                     const unsigned bo = __ballot_sync(0xffffffffu, open);

@@ -380,16 +380,15 @@ k_tri_density(const float* __restrict__ tri, uint64_t T, GridXf gx, const uint64
                 k = G.e0[2] + cidx / (ex * ey);
                 key = tri_box_sat(G.g, i, j, k);
             }
-            unsigned bal = __ballot_sync(0xffffffffu, key);
+            // every key lane searches its leaf at once (the searches' load latencies overlap)
+            const long long my_idx = key ? find_key(keys0, n0, morton3((uint32_t)i, (uint32_t)j, (uint32_t)k)) : -1;
+            unsigned bal = __ballot_sync(0xffffffffu, my_idx >= 0);
             while (bal) {
                 const int src = __ffs(bal) - 1;
                 bal &= bal - 1;
                 const int64_t vi = __shfl_sync(0xffffffffu, i, src), vj = __shfl_sync(0xffffffffu, j, src),
                               vk = __shfl_sync(0xffffffffu, k, src);
-                long long idx = -1;
-                if (lane == 0) idx = find_key(keys0, n0, morton3((uint32_t)vi, (uint32_t)vj, (uint32_t)vk));
-                idx = __shfl_sync(0xffffffffu, idx, 0);
-                if (idx < 0) continue;
+                const long long idx = __shfl_sync(0xffffffffu, my_idx, src);
                 // sub-voxels off the plane's slab are no hit; the others are queued and tested
                 // by the pinned SAT 32 at a time
                 int nq = 0;
