@@ -63,6 +63,11 @@ def test_create_validation_without_gpu(P):
     assert L.vox_create(C.byref(h), 64, bb, C.byref(opt)) == 1
     opt = P._Options(None, 0, 1, 0, 3, 16, 0, 0)                 # only 32 slices
     assert L.vox_create(C.byref(h), 64, bb, C.byref(opt)) == 1
+    opt = P._Options(None, 0, 1, 0, 3, 32, 0, 0, 0, 0, (3 << 30) + 1)   # part_candidates > 3*2^30
+    assert L.vox_create(C.byref(h), 64, bb, C.byref(opt)) == 1
+    opt = P._Options(None, 0, 1, 0, 3, 32, 0, 0, 0, 0, 1)       # one top cell per part: allowed
+    assert L.vox_create(C.byref(h), 64, bb, C.byref(opt)) == 0
+    L.vox_destroy(h)
     assert L.vox_create(C.byref(h), 64, bb, None) == 0           # no device work at create
     L.vox_destroy(h)
     assert P.lib().vox_status_str(5) == b"VOX_ERR_CAPACITY"
