@@ -430,7 +430,7 @@ __device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, floa
 
 // Warp per segment: its key voxels (the §4 predicate, as in emit), and for each key voxel the
 // 512 sub-voxels, 16 per lane: the §4 predicate on the 8x grid, with conservative shortcuts
-// (centre farther than R + sqrt(3)/2 + 0.25 fine voxels: no hit; the box within R - 0.25 of
+// (centre farther than R + sqrt(3)/2 + 0.1 fine voxels: no hit; the box within R - 0.1 of
 // the segment point nearest its centre: hit) that the pinned fp32 decision cannot contradict (its deviation
 // from the exact one is < 0.02 fine voxels at 8N <= 65536). The mask of each key voxel is
 // OR-ed into the level-0 masks (a key absent from level 0 = another shard: skipped).
@@ -461,7 +461,7 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
         far_consts(f.w, G.rg, iww, thr2);
         far_consts(f8.w, rg8, iww8, unused);
         // the centre is in the box: dist(segment, box) <= dist(segment, centre) and >= it - sqrt(3)/2
-        const float far = rg8 + 1.11602540378f, near = rg8 - 0.25f;   // margins 0.25 fine voxel
+        const float far = rg8 + 0.96602540378f, near = rg8 - 0.1f;   // margins 0.1 fine voxel
         const float far2 = far * far, near2 = near > 0.0f ? near * near : -1.0f;
         const int64_t ex = G.e1[0] - G.e0[0] + 1, ey = G.e1[1] - G.e0[1] + 1, ez = G.e1[2] - G.e0[2] + 1;
         const int64_t ncand = ex * ey * ez;

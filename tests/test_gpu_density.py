@@ -111,3 +111,34 @@ def test_density_states(P):
     v.density_fibers(S, R)
     v.build_lod(2)
     assert v.density_level(2)["occ"].numel() == v.view(2)["n"]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_density_fibers_at_max_coordinates(P, seed):
+    """Random fibers in the far corner of an 8192^3 grid (fine-grid coordinates near 8N =
+    65536, where fp32 spacing is coarsest), axis-parallel and oblique, radii 0 to 2 voxels:
+    the conservative sure-hit / sure-miss shortcuts of the density kernel never contradict
+    the pinned predicate (bit-exact masks against the oracle)."""
+    rng = np.random.default_rng(100 + seed)
+    n = 300
+    a = rng.uniform(0.996, 0.9995, (n, 3))
+    d = rng.normal(0, 1, (n, 3))
+    d[: n // 4, 1:] = 0.0                      # along x
+    d[n // 4: n // 3, :2] *= 1e-4               # nearly along z
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    b = a + d * rng.uniform(0.0, 6.0, (n, 1)) / 8192
+    s = np.stack([a, b], 1).astype(np.float32)
+    r = (rng.uniform(0.0, 2.0, n) / 8192).astype(np.float32)
+    bbox = np.array([0, 0, 0, 1, 1, 1], np.float32)
+    v = P.Vox(8192, bbox)
+    S, R = torch.from_numpy(s).cuda(), torch.from_numpy(r).cuda()
+    v.voxelize_fibers(S, R)
+    v.build_lod(1)
+    v.density_fibers(S, R)
+    o = oracle.Oracle(8192, bbox)
+    o.add_fibers(s, r)
+    o.build(1)
+    o.density_fibers(s, r)
+    _cmp(v, o, 0, tag=f"corner{seed}")
+    _cmp(v, o, 1, tag=f"corner{seed}")
+    assert float(v.density_level(0)["occ"].max()) > 0.1

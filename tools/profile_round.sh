@@ -23,5 +23,6 @@ cap() {   # cap <kernel regex> <name> <command...>
 for k in k_sggxh_quad k_sggxh_half k_sggxh_warp k_fiber_emit k_bin_reduce_warp k_lod_prep_leaf; do cap $k $k $B; done
 cap k_encode k_encode python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e
 cap k_spline_emit k_spline_emit $B --sampled 8
+cap k_fiber_density k_fiber_density python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e
 cap k_sggxh_hist k_sggxh_hist python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-finalize --config 2 --distance hist
 ls -la $OUT
