@@ -434,7 +434,7 @@ __device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, floa
 // the segment point nearest its centre: hit) that the pinned fp32 decision cannot contradict (its deviation
 // from the exact one is < 0.02 fine voxels at 8N <= 65536). The mask of each key voxel is
 // OR-ed into the level-0 masks (a key absent from level 0 = another shard: skipped).
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g,
                 const uint64_t* __restrict__ keys0, uint64_t n0, unsigned long long* __restrict__ masks) {
     __shared__ unsigned s_m[8][16];        // per warp: the voxel's 512-bit mask

@@ -343,7 +343,7 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
 // lane) by the §6 SAT on the 8x grid, skipping (no hit) sub-voxels whose centre is farther
 // than sqrt(3)/2 + 0.25 fine voxels from the triangle's plane (GPU-only shortcut; the pinned
 // SAT cannot report overlap there).
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 k_tri_density(const float* __restrict__ tri, uint64_t T, GridXf gx, const uint64_t* __restrict__ keys0,
               uint64_t n0, unsigned long long* __restrict__ masks) {
     __shared__ unsigned s_m[8][16];        // per warp: the voxel's 512-bit mask

@@ -395,14 +395,15 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     // the previous part's in key order, so the parts' leaf sets are concatenated.
     const uint64_t lo0 = c->cell_lo, hi0 = c->cell_hi;
     std::vector<uint64_t> cuts = {lo0, hi0};
+    unsigned long long* off1 = nullptr;   // offsets of the whole range, re-used by a single part
+    uint64_t cap1 = 0;
     {
-        unsigned long long* off = nullptr;
-        uint64_t cap = 0;
-        s = bin_offsets(c, Wb, Lb, &off, &cap);
+        s = bin_offsets(c, Wb, Lb, &off1, &cap1);
         if (s != VOX_OK) { dfree(c, Wb); return s; }
-        dfree(c, off);
-        c->st.candidates = cap;
-        if (cap > c->part_cand) {
+        c->st.candidates = cap1;
+        if (cap1 > c->part_cand) {
+            dfree(c, off1);
+            off1 = nullptr;
             std::vector<uint64_t> W;
             s = bin_topcells(c, Wb, Lb, W);
             if (s != VOX_OK) { dfree(c, Wb); return s; }
@@ -425,10 +426,14 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
     }
     c->st.pairs = 0;
     auto run_part = [&]() -> vox_status {
-        unsigned long long* off = nullptr;
-        uint64_t cap = 0;
-        vox_status r = bin_offsets(c, Wb, Lb, &off, &cap);
-        if (r != VOX_OK) return r;
+        unsigned long long* off = off1;
+        uint64_t cap = cap1;
+        vox_status r = VOX_OK;
+        if (!off) {
+            r = bin_offsets(c, Wb, Lb, &off, &cap);
+            if (r != VOX_OK) return r;
+        }
+        off1 = nullptr;   // owned (and freed) by this part from here
         if (cap == 0) {
             dfree(c, off);
             return VOX_OK;
