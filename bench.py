@@ -441,7 +441,8 @@ def main():
             top = levels if world == 1 else min(levels, int(math.log2(N)) - int(v.stats()["top_depth"]))
             dens = [v.density_level(l) for l in range(top + 1)]   # sharded: masks are per shard
             st = v.stats()
-            line["density"] = {"ms": st["ms_density"], "leaf_voxels": V[0],
+            line["density"] = {"ms": st["ms_density"], "host_ms_alloc": st["host_ms_alloc"],
+                               "host_ms_sync": st["host_ms_sync"], "leaf_voxels": V[0],
                                "sub_voxel_tests_per_leaf": 512,
                                "leaf_voxels_per_s": V[0] / (st["ms_density"] / 1e3),
                                "bound": "alu (pinned capsule-box predicate on the 8N grid for boundary sub-voxels)"}

