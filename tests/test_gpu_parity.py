@@ -201,8 +201,8 @@ def test_fake_world_sharding_equals_unsharded(P):
     full = P.Vox(N, [0, 0, 0, 1, 1, 1])
     full.voxelize_fibers(S, R)
     full.build_lod(L)
-    for world in (2, 3, 8):
-        shards = [P.Vox(N, [0, 0, 0, 1, 1, 1], rank=q, world=world) for q in range(world)]
+    for world, part in ((2, 0), (3, 0), (8, 0), (3, 20000)):   # part: Morton parts inside each shard
+        shards = [P.Vox(N, [0, 0, 0, 1, 1, 1], rank=q, world=world, part_candidates=part) for q in range(world)]
         for v in shards:
             v.voxelize_fibers(S, R)
             v.build_lod(L)                      # stops at log2(N) - T without the gather
