@@ -414,20 +414,6 @@ __device__ __forceinline__ void fib_setup(Fib& f, float (&d)[3], const float* a,
     f.len = sqrtf(ss);
 }
 
-// centre distance^2 of fine voxel (x,y,z) to the segment, and (box2) the squared distance from
-// the segment point nearest the centre to the box (GPU-only shortcut geometry: the
-// segment-box distance lies in [sqrt(c2) - sqrt(3)/2, sqrt(box2)])
-__device__ __forceinline__ float centre_dist2(const Fib& f, const float* d, float iww, int64_t x, int64_t y, int64_t z,
-                                              float& box2) {
-    const float e0 = ((float)x + 0.5f) - f.a[0], e1 = ((float)y + 0.5f) - f.a[1], e2 = ((float)z + 0.5f) - f.a[2];
-    float t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) * iww;   // iww = 1 / |d|^2 (0 for a sphere)
-    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
-    const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
-    const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f), o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
-    box2 = o0 * o0 + o1 * o1 + o2 * o2;
-    return q0 * q0 + q1 * q1 + q2 * q2;
-}
-
 // Warp per segment: its key voxels (the §4 predicate, as in emit), and for each key voxel the
 // 512 sub-voxels, 16 per lane: the §4 predicate on the 8x grid, with conservative shortcuts
 // (centre farther than R + sqrt(3)/2 + 0.1 fine voxels: no hit; the box within R - 0.1 of
@@ -488,12 +474,28 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                 // classify the 512 sub-voxels (16 per lane): sure hits straight into the mask,
                 // undecided ones queued, then the queue evaluated 32 at a time (no divergence)
                 int nq = 0;
+                // c2 = squared distance of the sub-voxel centre to the segment, box2 = squared
+                // distance of the segment point nearest that centre to the sub-voxel box: the
+                // segment-box distance lies in [sqrt(c2) - sqrt(3)/2, sqrt(box2)].
+                // Centre offsets from the segment start: exact lattice offsets added to a per-voxel
+                // base (the shortcut is conservative geometry, so its rounding need not match the
+                // pinned predicate's; its error is far inside the 0.1 margin)
+                const float e0 = (((float)(8 * vi) + 0.5f) - f8.a[0]) + (float)(lane & 7);
+                const float e1a = (((float)(8 * vj) + 0.5f) - f8.a[1]) + (float)(lane >> 3);
+                const float e1b = e1a + 4.0f;
+                const float e2b = ((float)(8 * vk) + 0.5f) - f8.a[2];
+                const float pa = e0 * d8[0] + e1a * d8[1], pb = e0 * d8[0] + e1b * d8[1];
 #pragma unroll 1
                 for (int q = 0; q < 16; q++) {
                     const int sub = lane + 32 * q;
-                    const int64_t x = 8 * vi + (sub & 7), y = 8 * vj + ((sub >> 3) & 7), z = 8 * vk + (sub >> 6);
-                    float box2;
-                    const float c2 = centre_dist2(f8, d8, iww8, x, y, z, box2);
+                    const float e1 = (q & 1) ? e1b : e1a, e2 = e2b + (float)(q >> 1);
+                    float t = (((q & 1) ? pb : pa) + e2 * d8[2]) * iww8;
+                    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
+                    const float q0 = e0 - t * d8[0], q1 = e1 - t * d8[1], q2 = e2 - t * d8[2];
+                    const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f),
+                                o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
+                    const float box2 = o0 * o0 + o1 * o1 + o2 * o2;
+                    const float c2 = q0 * q0 + q1 * q1 + q2 * q2;
                     const bool sure = box2 < near2, open = !sure && !(c2 > far2);
                     const unsigned bs = __ballot_sync(0xffffffffu, sure);
                     const unsigned bo = __ballot_sync(0xffffffffu, open);
