@@ -251,7 +251,7 @@ __device__ __forceinline__ void eval_queue(const int4* q, int nq, int lane, floa
 // lane evaluates one (segment, voxel) candidate per step whatever the segment sizes.
 // Keys add q(l_r) into the segment's exact S_acc (shared int64); in-grid, in-shard keys are
 // compacted with a warp ballot and appended to the pair stream with one atomic per warp step.
-__global__ void __launch_bounds__(EMIT_WARPS * 32, 3)
+__global__ void __launch_bounds__(EMIT_WARPS * 32, 4)
 k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g, Shard sh,
              Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals, float4* __restrict__ ptab,
              unsigned* __restrict__ flags) {
