@@ -2,7 +2,9 @@
 # tools/profile_round.sh <out dir> -- run ON THE GPU BOX: launch list with DRAM bytes of one
 # bench step, and ncu --set full captures of the hot kernels, summarised in place (the
 # .ncu-rep files are deleted after summarising so the directory stays small).
+# Optional second argument: a space-separated list of kernels to capture (default: all).
 OUT=$1
+ONLY=${2:-}
 mkdir -p $OUT
 B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-finalize"
 $B > $OUT/plain.log 2>&1 || exit 1
@@ -11,6 +13,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 python3 tools/launch_traffic.py $OUT/launches.csv > $OUT/traffic.json
 cap() {   # cap <kernel regex> <name> <command...>
   local k=$1 n=$2; shift 2
+  if [ -n "$ONLY" ] && [[ " $ONLY " != *" $n "* ]]; then return; fi
   ncu --set full --clock-control none --import-source on -k regex:$k -s 0 -c 1 -o $OUT/$n "$@" > $OUT/ncu_$n.log 2>&1
   if [ -f $OUT/$n.ncu-rep ]; then
     python3 tools/ncu_summary.py $OUT/$n.ncu-rep "$n" > $OUT/$n.md
