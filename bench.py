@@ -107,48 +107,125 @@ def _cells_by_count(seg, bbox, N, level):
     return u[order], cnt[order]
 
 
-def oracle_sample(c, target_segments: int, level: int, distance: str = "sigma", hist_samples: int = 5000):
-    """Time the oracle (single-threaded, as it stands) on whole Morton cells at `level`,
-    largest first, until `target_segments` segments have been processed: every segment
-    touching a cell is voxelized (its S_p needs all its keys) and the LoD is built inside the
-    cell up to `level`. Returns (segments processed, seconds, description)."""
-    import oracle
+def _cell_inputs(c, level):
+    """Morton cells at `level`, largest first, each with every segment whose box touches it."""
     seg, rad, bbox, N = c["segments"], c["radii"], c["bbox"], c["grid_res"]
     E = float(np.max(bbox[3:] - bbox[:3]))
     lo = np.minimum(seg[:, 0], seg[:, 1]) - rad[:, None]
     hi = np.maximum(seg[:, 0], seg[:, 1]) + rad[:, None]
     cells, _ = _cells_by_count(seg, bbox, N, level)
-    done, secs, used = 0, 0.0, []
+    import oracle
     for cell in cells:
         i, j, k = oracle.unmorton(int(cell))
         box_lo = np.array([i, j, k], np.float64) * (1 << level) * E / N + bbox[:3] - 2 * E / N
         box_hi = box_lo + ((1 << level) + 4) * E / N
         sel = np.all((hi >= box_lo) & (lo <= box_hi), axis=1)
-        s, r = np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
-        o = oracle.Oracle(N, bbox, distance=distance, hist_samples=hist_samples)
-        o.set_window(level, int(cell))
-        t0 = time.perf_counter()
-        o.add_fibers(s, r)
-        o.build(level)
-        secs += time.perf_counter() - t0
-        done += len(s)
-        used.append(int(cell))
-        o.close()
-        if done >= target_segments:
-            break
-    desc = (f"oracle (plain C, 1 thread, {distance} distance) on {len(used)} Morton cell(s) at level {level} "
-            f"({1 << level}^3 voxels each): {done} segments touching them voxelized + LoD levels 1..{level} "
-            f"inside them")
-    return done, secs, desc
+        yield int(cell), np.ascontiguousarray(seg[sel]), np.ascontiguousarray(rad[sel])
+
+
+def _oracle_cell(N, bbox, level, cell, s, r, distance, hist_samples):
+    """One oracle run (voxelize + LoD inside one Morton cell); returns (segments, seconds,
+    digest of every level's keys, accumulators and lobes). Module level: it runs in worker
+    processes for the all-cores sample."""
+    import hashlib
+    sys.path.insert(0, ROOT)
+    import oracle
+    o = oracle.Oracle(N, bbox, distance=distance, hist_samples=hist_samples)
+    o.set_window(level, cell)
+    t0 = time.perf_counter()
+    o.add_fibers(s, r)
+    o.build(level)
+    dt = time.perf_counter() - t0
+    h = hashlib.sha256()
+    for l in range(level + 1):
+        L = o.level(l)
+        h.update(L["key"].tobytes())
+        h.update(L["acc"].tobytes())
+        if l > 0:
+            h.update(L["cl"].tobytes())
+    o.close()
+    return len(s), dt, h.hexdigest()
+
+
+def _oracle_job(a):
+    return _oracle_cell(*a)
+
+
+def _warm(_):
+    sys.path.insert(0, ROOT)
+    import oracle
+    oracle.lib()
+    return 0
+
+
+def oracle_sample(c, target_segments: int, level: int, distance: str = "sigma", hist_samples: int = 5000,
+                  threads: int = 1, n_cells: int = 0):
+    """Time the oracle (as it stands: plain C, no tuning) on whole Morton cells at `level`,
+    largest first: every segment touching a cell is voxelized (its S_p needs all its keys) and
+    the LoD is built inside the cell up to `level`. threads == 1: cells one after another until
+    `target_segments` segments; threads > 1: the first `n_cells` cells, one oracle per cell on a
+    pool of `threads` host threads (wall time). Returns (segments, seconds, description, digests
+    per cell)."""
+    import concurrent.futures as cf
+    done, secs, used, digests = 0, 0.0, [], []
+    N, bbox = c["grid_res"], c["bbox"]
+    if threads <= 1:
+        for cell, s, r in _cell_inputs(c, level):
+            n, dt, dg = _oracle_cell(N, bbox, level, cell, s, r, distance, hist_samples)
+            done += n
+            secs += dt
+            used.append(cell)
+            digests.append(dg)
+            if done >= target_segments:
+                break
+    else:
+        jobs = []
+        for cell, s, r in _cell_inputs(c, level):
+            jobs.append((cell, s, r))
+            if len(jobs) >= n_cells:
+                break
+        threads = min(threads, len(jobs))
+        import multiprocessing as mp
+        # one process per host core (the C oracle is single-threaded; processes avoid the
+        # allocator contention threads showed); workers are started before the clock
+        with cf.ProcessPoolExecutor(threads, mp_context=mp.get_context("spawn")) as ex:
+            list(ex.map(_warm, range(threads)))
+            t0 = time.perf_counter()
+            res = list(ex.map(_oracle_job, [(N, bbox, level, j[0], j[1], j[2], distance, hist_samples)
+                                            for j in jobs]))
+            secs = time.perf_counter() - t0
+        done = sum(x[0] for x in res)
+        used = [j[0] for j in jobs]
+        digests = [x[2] for x in res]
+    desc = (f"oracle (plain C, {threads} host process{'es' if threads > 1 else ''}, {distance} distance) on "
+            f"{len(used)} Morton cell(s) at level {level} ({1 << level}^3 voxels each): {done} segments touching "
+            f"them voxelized + LoD levels 1..{level} inside them")
+    return done, secs, desc, digests
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores, bounded samples."""
     c = _workload(args.config, args.segments)
     lvl = 7 if c["grid_res"] >= 2048 else max(1, int(math.log2(c["grid_res"])) - 2)
-    times, counts, desc = [], [], ""   # each step: one bounded oracle sample (~1-3 s)
+    times, counts, desc = [], [], ""   # each step: one bounded oracle sample, every host core
+    ncpu = os.cpu_count() or 1
+    thr = 1
     for it in range(args.warmup + args.steps):
-        n, dt, desc = oracle_sample(c, args.ref_segments, lvl)
+        if ncpu > 1:
+            n, dt, desc, dg = oracle_sample(c, 0, lvl, threads=ncpu, n_cells=min(ncpu, args.cpu_cells))
+            thr = min(ncpu, len(dg))
+        else:
+            n, dt, desc, _ = oracle_sample(c, args.ref_segments, lvl)
         if it >= args.warmup:
             times.append(dt)
             counts.append(n)
@@ -157,7 +234,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": f"config {args.config} sample: {desc}"},
-            "cpu_baseline": {"value": value, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "segments/s", "cores": thr, "kind": "oracle", "sample": desc,
+                             "host_cpus": ncpu, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "segments/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -180,13 +258,26 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-finalize", action="store_true", help="skip the compact-form (NEXT-3) measurement")
-    ap.add_argument("--cpu-segments", type=int, default=400_000, help="oracle sample size (cpu_baseline)")
+    ap.add_argument("--cpu-segments", type=int, default=200_000, help="oracle sample size, 1 thread (cpu_baseline)")
+    ap.add_argument("--cpu-cells", type=int, default=64, help="cells of the all-cores oracle sample (cpu_baseline)")
     ap.add_argument("--ref-segments", type=int, default=40_000, help="oracle sample size per reference step")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun with N ranks
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         if rank == 0:
             run_reference(args)
@@ -197,6 +288,8 @@ def main():
 
     from paper_2604_13191_b200 import Vox, build as vbuild
     vbuild.build()
+    if torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     group = None
     if world > 1:
@@ -372,26 +465,37 @@ def main():
 
         copy_stream = torch.cuda.Stream()
 
+        lt = int(math.log2(N)) - 4 if world > 1 else -1   # the gathered level (top_depth 4)
+
+        def copy_out(v, l):
+            """vox_copy_level_async of level l into pinned host buffers; returns its bytes."""
+            n_l = int(v.view(l)["n"])
+            if l not in host or host[l]["key"].numel() < n_l:
+                host[l] = {"key": torch.empty(n_l, dtype=torch.int64).pin_memory(),
+                           "mass": torch.empty(n_l, dtype=torch.float32).pin_memory(),
+                           "m6": torch.empty(n_l * 6, dtype=torch.float32).pin_memory()}
+                if l > 0:
+                    host[l]["ncl"] = torch.empty(n_l, dtype=torch.uint8).pin_memory()
+                    host[l]["cl"] = torch.empty(n_l * v.k * 7, dtype=torch.float32).pin_memory()
+            v.copy_level_async(l, host[l], copy_stream)
+            return n_l * (8 + 4 + 24 + ((1 + 28 * v.k) if l > 0 else 0))
+
         def e2e_step():
             v = Vox(N, bbox, rank=rank, world=world, distance=args.distance, hist_samples=args.hist_samples)
             if fib:
                 v.voxelize_fibers_host(pa, pb)
             else:
                 v.voxelize_triangles_host(pa, pb)
-            d2h = 0
-            # build level by level; each finished level's D2H runs on a second stream while the
-            # next levels are built (vox_copy_level_async: event-ordered, no sync)
+            # the leaf level (the voxelization itself, P:248-257) first, then level by level;
+            # each finished level's D2H runs on a second stream while the next levels are built
+            # (vox_copy_level_async: event-ordered, no sync)
+            d2h = copy_out(v, 0)
             for l in range(1, levels + 1):
                 v.build_lod(l, group)
-                n_l = int(v.view(l)["n"])
-                if l not in host or host[l]["key"].numel() < n_l:
-                    host[l] = {"key": torch.empty(n_l, dtype=torch.int64).pin_memory(),
-                               "mass": torch.empty(n_l, dtype=torch.float32).pin_memory(),
-                               "m6": torch.empty(n_l * 6, dtype=torch.float32).pin_memory(),
-                               "ncl": torch.empty(n_l, dtype=torch.uint8).pin_memory(),
-                               "cl": torch.empty(n_l * v.k * 7, dtype=torch.float32).pin_memory()}
-                v.copy_level_async(l, host[l], copy_stream)
-                d2h += n_l * (8 + 4 + 24 + 1 + 28 * v.k)
+                if l != lt:          # sharded: level lt is copied once gathered (below)
+                    d2h += copy_out(v, l)
+            if 0 < lt <= levels:
+                d2h += copy_out(v, lt)
             copy_stream.synchronize()
             v.close()
             outs["d2h"] = d2h
@@ -451,12 +555,26 @@ def main():
         del bufs
 
     # ---------------------------------------------------------------- CPU baseline (oracle), rank 0, N = 1
+    # the oracle as it stands, on the box's host cores: one thread on the densest cell(s), then
+    # one oracle per cell on every core (ctypes releases the GIL); the cells both runs share
+    # must give bit-identical levels
     if rank == 0 and world == 1 and not args.no_cpu_baseline and fib and not args.sampled:
         lvl = 9 if N >= 4096 else max(1, int(math.log2(N)) - 3)
         target = args.cpu_segments if args.distance == "sigma" else max(1000, args.cpu_segments // 100)
-        n, dt, desc = oracle_sample(c, target, lvl, args.distance, args.hist_samples)
-        line["cpu_baseline"] = {"value": n / dt, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc,
-                                "seconds": dt}
+        n1, dt1, desc1, dg1 = oracle_sample(c, target, lvl, args.distance, args.hist_samples)
+        ncpu = os.cpu_count() or 1
+        cb = {"value": n1 / dt1, "unit": "segments/s", "cores": 1, "kind": "oracle", "sample": desc1,
+              "seconds": dt1, "host_cpus": ncpu, "cpu_model": _cpu_model()}
+        if ncpu > 1 and args.distance == "sigma":
+            ncell = max(len(dg1), min(ncpu, args.cpu_cells))
+            nm, dtm, descm, dgm = oracle_sample(c, 0, lvl, args.distance, args.hist_samples, threads=ncpu,
+                                                n_cells=ncell)
+            thr = min(ncpu, len(dgm))
+            cb = {"value": nm / dtm, "unit": "segments/s", "cores": thr, "kind": "oracle", "sample": descm,
+                  "seconds": dtm, "host_cpus": ncpu, "cpu_model": _cpu_model(),
+                  "bit_identical_to_1_thread": dgm[:len(dg1)] == dg1,
+                  "one_thread": {"value": n1 / dt1, "cores": 1, "sample": desc1, "seconds": dt1}}
+        line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -116,17 +116,18 @@ __global__ void k_peek(const unsigned* __restrict__ src, unsigned* __restrict__ 
 }
 
 static std::mutex g_map_mu;
-static std::vector<std::pair<void*, void*>> g_map_pool;   // (host, device) mapped pinned blocks
+static std::map<int, std::vector<std::pair<void*, void*>>> g_map_pool;   // per device: (host, device alias)
 constexpr size_t MAP_BYTES = 64 * 1024;
 
 static cudaError_t acquire_mapped(vox_ctx* c) {
     if (c->h_map) return cudaSuccess;
     {
         std::lock_guard<std::mutex> lk(g_map_mu);
-        if (!g_map_pool.empty()) {
-            c->h_map = g_map_pool.back().first;
-            c->d_map = g_map_pool.back().second;
-            g_map_pool.pop_back();
+        std::vector<std::pair<void*, void*>>& pool = g_map_pool[c->dev];
+        if (!pool.empty()) {
+            c->h_map = pool.back().first;
+            c->d_map = pool.back().second;
+            pool.pop_back();
             return cudaSuccess;
         }
     }
@@ -138,7 +139,7 @@ static cudaError_t acquire_mapped(vox_ctx* c) {
 static void release_mapped(vox_ctx* c) {
     if (!c->h_map) return;
     std::lock_guard<std::mutex> lk(g_map_mu);
-    g_map_pool.push_back({c->h_map, c->d_map});
+    g_map_pool[c->dev].push_back({c->h_map, c->d_map});
     c->h_map = c->d_map = nullptr;
 }
 
@@ -167,6 +168,13 @@ cudaError_t readback(vox_ctx* c, std::initializer_list<ReadItem> items) {
 }
 
 void free_level(vox_ctx* c, Level& L) {
+    if (&L >= c->lv && &L < c->lv + VOX_MAX_LEVELS) {
+        const int l = (int)(&L - c->lv);
+        if (c->ev_read_pending[l]) {   // an async copy of this level may still be reading it
+            cudaStreamWaitEvent(c->stream, c->ev_read[l], 0);
+            c->ev_read_pending[l] = false;
+        }
+    }
     dfree(c, L.key); dfree(c, L.acc); dfree(c, L.mass); dfree(c, L.m6);
     dfree(c, L.ncl); dfree(c, L.clacc); dfree(c, L.cl);
     L = Level();
@@ -175,7 +183,7 @@ void free_level(vox_ctx* c, Level& L) {
 // Timing events are recycled process-wide: creating events costs tens of microseconds,
 // which would add up over the ~200 stage events of one voxelize + LoD build.
 static std::mutex g_ev_mu;
-static std::vector<cudaEvent_t> g_ev_pool;
+static std::map<int, std::vector<cudaEvent_t>> g_ev_pool;   // per device: events are device-bound
 
 static cudaEvent_t event_get(vox_ctx* c) {
     if (!c->ev_pool.empty()) {
@@ -185,27 +193,43 @@ static cudaEvent_t event_get(vox_ctx* c) {
     }
     {
         std::lock_guard<std::mutex> lk(g_ev_mu);
-        if (!g_ev_pool.empty()) {
-            cudaEvent_t e = g_ev_pool.back();
-            g_ev_pool.pop_back();
+        std::vector<cudaEvent_t>& pool = g_ev_pool[c->dev];
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
             return e;
         }
     }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
     return e;
 }
 
+// Timing is best effort: a failed event creation or record drops the sample and clears the
+// error, so it can never surface later as a launcher's VOX_ERR_CUDA.
 void timer_begin(vox_ctx* c, StageTimer& t) {
     if (!c->profile) return;
     t.open = event_get(c);
-    cudaEventRecord(t.open, c->stream);
+    if (t.open && cudaEventRecord(t.open, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        c->ev_pool.push_back(t.open);
+        t.open = nullptr;
+    }
 }
 
 void timer_end(vox_ctx* c, StageTimer& t) {
     if (!c->profile || !t.open) return;
     cudaEvent_t b = event_get(c);
-    cudaEventRecord(b, c->stream);
+    if (!b || cudaEventRecord(b, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        c->ev_pool.push_back(t.open);
+        if (b) c->ev_pool.push_back(b);
+        t.open = nullptr;
+        return;
+    }
     t.done.emplace_back(t.open, b);
     t.open = nullptr;
 }
@@ -317,6 +341,10 @@ vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], con
     c->part_cand = o.part_candidates;
     c->built = 0;
     c->st.top_depth = (uint32_t)c->T;
+    if (cudaGetDevice(&c->dev) != cudaSuccess) {
+        cudaGetLastError();
+        c->dev = 0;
+    }
     *out = c;
     return VOX_OK;
 }
@@ -855,6 +883,10 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
     CKS(cudaEventDestroy(ev));
     if (ncl) CKS(cudaMemcpyAsync(ncl, L.ncl, n, cudaMemcpyDefault, s));
     if (cl) CKS(cudaMemcpyAsync(cl, L.cl, n * c->K * 28, cudaMemcpyDefault, s));
+    // the level's arrays are being read on `s` until here: free_level / import wait on it
+    if (!c->ev_read[level]) CKS(cudaEventCreateWithFlags(&c->ev_read[level], cudaEventDisableTiming));
+    CKS(cudaEventRecord(c->ev_read[level], s));
+    c->ev_read_pending[level] = true;
     return VOX_OK;
 }
 
@@ -891,6 +923,14 @@ vox_status vox_import_level(vox_ctx* c, uint32_t level, const void* buf, uint64_
     if (s != VOX_OK) return s;
     for (int l = (int)level + 1; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
     for (int l = (int)level; l < VOX_MAX_LEVELS; l++) c->ev_level_ok[l] = false;   // arrays replaced
+    // sub-voxel masks of the replaced levels were sized for the old arrays: drop them (the
+    // masks are per shard and are not exchanged, vox_density_level refuses gathered levels)
+    for (int l = (int)level; l < VOX_MAX_LEVELS; l++)
+        if (c->dmask[l]) {
+            dfree(c, c->dmask[l]);
+            c->dmask[l] = nullptr;
+        }
+    if (c->dmask_levels >= (int)level) c->dmask_levels = (int)level - 1;
     s = unpack_level(c, (int)level, buf, bytes / rb);
     if (s != VOX_OK) return s;
     c->imported_level = (int)level;
@@ -982,9 +1022,11 @@ void vox_destroy(vox_ctx* c) {
     ssync(c);
     release_mapped(c);
     density_reset(c);
-    for (int l = 0; l < VOX_MAX_LEVELS; l++)
-        if (c->ev_level[l]) cudaEventDestroy(c->ev_level[l]);
     for (int l = 0; l < VOX_MAX_LEVELS; l++) free_level(c, c->lv[l]);
+    for (int l = 0; l < VOX_MAX_LEVELS; l++) {
+        if (c->ev_level[l]) cudaEventDestroy(c->ev_level[l]);
+        if (c->ev_read[l]) cudaEventDestroy(c->ev_read[l]);
+    }
     for (StageTimer* t : {&c->t_bound, &c->t_emit, &c->t_sort, &c->t_reduce, &c->t_merge, &c->t_lodscan, &c->t_lod,
                           &c->t_vox, &c->t_lodall, &c->t_prep, &c->t_quad, &c->t_half, &c->t_warp, &c->t_encode, &c->t_density}) {
         timer_flush(c, *t);
@@ -992,7 +1034,7 @@ void vox_destroy(vox_ctx* c) {
     }
     {
         std::lock_guard<std::mutex> lk(g_ev_mu);
-        for (cudaEvent_t e : c->ev_pool) g_ev_pool.push_back(e);
+        for (cudaEvent_t e : c->ev_pool) g_ev_pool[c->dev].push_back(e);
     }
     c->ev_pool.clear();
     if (c->d_lodwork) cudaFreeAsync(c->d_lodwork, c->stream);

@@ -193,6 +193,12 @@ struct vox_ctx {
     int dmask_levels = -1;                  // levels with valid masks (0 after vox_density_*)
     cudaEvent_t ev_level[VOX_MAX_LEVELS] = {};   // recorded when a level's key/mass/m6 are final
     bool ev_level_ok[VOX_MAX_LEVELS] = {};
+    // recorded on the caller's stream after a vox_copy_level_async of the level: freeing or
+    // replacing the level's arrays first makes the ctx stream wait on it (the arrays go back to
+    // the stream-keyed block cache and would otherwise be reused under the pending copy)
+    cudaEvent_t ev_read[VOX_MAX_LEVELS] = {};
+    bool ev_read_pending[VOX_MAX_LEVELS] = {};
+    int dev = 0;                            // device of the ctx (event pool key)
     void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
     void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)

@@ -20,6 +20,11 @@ def gather_varlen(buf: torch.Tensor, group=None) -> torch.Tensor:
     buffers padded to the longest one.
     """
     world = dist.get_world_size(group)
+    dev = buf.device
+    if dev.type == "cuda" and dist.get_backend(group) == "gloo":
+        # gloo collectives run on host memory: stage the records through the CPU (used by the
+        # multi-process tests on one GPU; NCCL moves device buffers directly over NVLink)
+        return gather_varlen(buf.cpu(), group).to(dev)
     n = torch.tensor([buf.numel()], dtype=torch.int64, device=buf.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)

@@ -201,6 +201,13 @@ def test_fake_world_sharding_equals_unsharded(P):
     full = P.Vox(N, [0, 0, 0, 1, 1, 1])
     full.voxelize_fibers(S, R)
     full.build_lod(L)
+    # anchor: the unsharded result is the oracle's, level by level (so every comparison of the
+    # shards with `full` below is a comparison with the oracle)
+    o = oracle.Oracle(N, np.array([0, 0, 0, 1, 1, 1], np.float32))
+    o.add_fibers(s, r)
+    o.build(L)
+    for l in range(L + 1):
+        _cmp_level(full.level(l), o.level(l), l, "unsharded weave")
     for world, part in ((2, 0), (3, 0), (8, 0), (3, 20000)):   # part: Morton parts inside each shard
         shards = [P.Vox(N, [0, 0, 0, 1, 1, 1], rank=q, world=world, part_candidates=part) for q in range(world)]
         for v in shards:
@@ -232,6 +239,11 @@ def test_fake_world_triangles(P):
     full = P.Vox(c["grid_res"], c["bbox"])
     full.voxelize_triangles(T)
     full.build_lod(c["levels"])
+    o = oracle.Oracle(c["grid_res"], c["bbox"])
+    o.add_triangles(c["tris"])
+    o.build(c["levels"])
+    for l in range(c["levels"] + 1):
+        _cmp_level(full.level(l), o.level(l), l, "unsharded icosphere")
     for world in (2, 5):
         shards = [P.Vox(c["grid_res"], c["bbox"], rank=q, world=world) for q in range(world)]
         for v in shards:
