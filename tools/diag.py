@@ -1,0 +1,118 @@
+"""Diagnostics on a GPU box (not part of the product or the tests).
+
+    python tools/diag.py stages  [segments]        per-stage device times of config 4 (profile mode)
+    python tools/diag.py nhist                     per-level histogram of SGGX-H lobe counts n > K, kernel times
+    python tools/diag.py shard   [world ...]       per-rank device time of config-4 Morton shards, one GPU
+    python tools/diag.py maxsize [segments] [N]    config 5 point: device time, counts, memory
+    python tools/diag.py density [segments]        device time of the sub-voxel density pass (NEXT-2)
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from paper_2604_13191_b200 import Vox  # noqa: E402
+
+
+def _dev(c):
+    return torch.from_numpy(c["segments"]).cuda(), torch.from_numpy(c["radii"]).cuda()
+
+
+def stages(n=10_000_000):
+    c = gen.config(4, n_segments=int(n))
+    S, R = _dev(c)
+    acc = {}
+    for it in range(5):
+        v = Vox(c["grid_res"], c["bbox"], profile=True)
+        v.voxelize_fibers(S, R)
+        v.build_lod(c["levels"])
+        st = v.stats()
+        v.close()
+        if it >= 2:
+            for k, x in st.items():
+                if k.startswith("ms_"):
+                    acc[k] = acc.get(k, 0) + x / 3
+    print({k: round(x, 3) for k, x in acc.items()})
+
+
+def nhist():
+    c = gen.config(4)
+    S, R = _dev(c)
+    v = Vox(c["grid_res"], c["bbox"], profile=True)
+    v.voxelize_fibers(S, R)
+    prev = v.level(0)
+    for l in range(1, c["levels"] + 1):
+        v.stats_reset()
+        v.build_lod(l)
+        st = v.stats()
+        cur = v.level(l)
+        pk = prev["key"] >> 3
+        lob = prev["ncl"].long() if l > 1 else (prev["acc"][:, 0] > 0).long()
+        idx = torch.searchsorted(cur["key"], pk)
+        n = torch.zeros(len(cur["key"]), dtype=torch.long, device="cuda").index_add_(0, idx, lob)
+        h = torch.bincount(n[n > v.k], minlength=25).cpu().tolist()
+        print(l, "parents", len(n), "hard", int((n > v.k).sum()),
+              {k: round(st[k], 2) for k in ("ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_half", "ms_sggxh_warp")},
+              {k: x for k, x in enumerate(h) if x}, flush=True)
+        prev = cur
+
+
+def shard(*worlds):
+    c = gen.config(4)
+    S, R = _dev(c)
+    for world in [int(x) for x in (worlds or (1, 2, 4, 8))]:
+        worst = 0.0
+        for rank in range(world):
+            for _ in range(2):
+                v = Vox(c["grid_res"], c["bbox"], rank=rank, world=world, profile=True)
+                v.voxelize_fibers(S, R)
+                v.build_lod(c["levels"])
+                st = v.stats()
+                v.close()
+            t = st["ms_total_vox"] + st["ms_total_lod"]
+            worst = max(worst, t)
+            print(world, "rank", rank, "cells", st["cell_lo"], st["cell_hi"], "emit", round(st["ms_emit"], 2),
+                  "vox", round(st["ms_total_vox"], 2), "lod", round(st["ms_total_lod"], 2), flush=True)
+        print(world, "max over ranks", round(worst, 2), "ms", flush=True)
+
+
+def maxsize(n=15_000_000, N=8192):
+    t0 = time.time()
+    c = gen.config(5, n_segments=int(n), grid_res=int(N))
+    print("generated", len(c["segments"]), "segments in", round(time.time() - t0, 1), "s", flush=True)
+    S, R = _dev(c)
+    for _ in range(2):
+        v = Vox(c["grid_res"], c["bbox"], profile=True)
+        v.voxelize_fibers(S, R)
+        v.build_lod(c["levels"])
+        st = v.stats()
+        print({k: round(st[k], 1) for k in ("ms_total_vox", "ms_total_lod")}, "pairs", st["pairs"],
+              "cand", st["candidates"], "leaves", st["voxels"],
+              "peak GB", round(torch.cuda.max_memory_allocated() / 1e9, 1),
+              "free GB", round(torch.cuda.mem_get_info()[0] / 1e9, 1), flush=True)
+        v.close()
+
+
+def density(n=10_000_000):
+    c = gen.config(4, n_segments=int(n))
+    S, R = _dev(c)
+    for _ in range(3):
+        v = Vox(c["grid_res"], c["bbox"], profile=True)
+        v.voxelize_fibers(S, R)
+        v.build_lod(c["levels"])
+        v.stats_reset()
+        v.density_fibers(S, R)
+        for l in range(c["levels"] + 1):
+            v.density_level(l)
+        st = v.stats()
+        print("density ms", round(st["ms_density"], 2), "alloc ms", round(st["host_ms_alloc"], 2), flush=True)
+        v.close()
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1] if len(sys.argv) > 1 else "stages"
+    globals()[cmd](*sys.argv[2:])
