@@ -352,11 +352,13 @@ def main():
             lodwork["sigma"] += st["lod_sigma_evals"]
             lodwork["dist"] += st["lod_dist_evals"]
             lodwork["hard"] += st["lod_hard_parents"]
-            counts = {"pairs": st["pairs"], "candidates": st["candidates"], "voxels": st["voxels"],
-                      "levels": [int(v.view(l)["n"]) for l in range(levels + 1)]}
-            v.close()
+            counts = {"pairs": st["pairs"], "candidates": st["candidates"], "voxels": st["voxels"]}
+            if _ + 1 < args.steps:
+                v.close()
         ev1.record(stream)
         torch.cuda.synchronize()
+    counts["levels"] = [v.size(l) for l in range(levels + 1)]
+    v.close()
     barrier()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -381,11 +383,15 @@ def main():
     bytes_vox = 28 * n_prims + 32 * P + 36 * V[0]
     bytes_lod = sum((36 * V[0] if l == 1 else 121 * V[l - 1]) + 121 * V[l] for l in range(1, levels + 1))
     sig_ev, dist_ev = lodwork["sigma"] / args.steps, lodwork["dist"] / args.steps
-    flops_sggxh = 416.0 * sig_ev + 95.0 * dist_ev      # PREDICATES §9: 32 x 13 per sigma, 32+32+31 per distance
+    # SURVEY §8(d) op model: 15 fp32 ops per sigma slice (6 mul, 5 add, max, sqrt counted as 3),
+    # 2 per slice of a distance (subtract, accumulate the absolute value); 32 slices
+    flops_sggxh = 32 * 15.0 * sig_ev + 32 * 2.0 * dist_ev
     emit_name = ("k_spline_emit" if fib else "k_tris_emit") if args.sampled else ("k_fiber_emit" if fib else "k_tri_emit")
     emit_bytes = (52 * n_prims + 32 * P) if (args.sampled and fib) else (28 * n_prims + 16 * P + 16 * n_prims)
+    # emit is issue-bound on the pinned predicate (ALU): its algorithmic bytes are reported, its
+    # fraction is not a bandwidth fraction (profiles/ carry the issue-slot utilisation)
     kern = {
-        emit_name: (stage["ms_emit"], "hbm", emit_bytes),
+        emit_name: (stage["ms_emit"], "alu-issue", emit_bytes),
         "k_bin_count": (stage["ms_sort"], "hbm", 8 * P),
         "k_bin_reduce": (stage["ms_reduce"], "hbm", 16 * P + 16 * n_prims + 64 * V[0]),
         "k_lod_prep": (stage["ms_lod_prep"], "hbm", bytes_lod),
@@ -406,12 +412,17 @@ def main():
             ach = work / dur / 1e9 if dur > 0 else None
             r = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)", "alg_bytes_per_launch": work}
+        elif bound == "alu-issue":
+            r = {"kernel": name, "bound": "alu", "achieved": None, "peak": None, "unit": "GB/s",
+                 "note": "issue-bound on the pinned predicate; algorithmic GB/s given, no lane-op count",
+                 "alg_gbs": work / dur / 1e9 if dur > 0 else None, "alg_bytes_per_launch": work}
         else:
             ach = work / dur / 1e12 if dur > 0 else None
             r = {"kernel": name, "bound": "alu", "achieved": ach, "peak": alu_peak_tflops, "unit": "TFLOP/s",
                  "peak_source": f"{nsm} SMs x 128 fp32 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz; no FMA)",
-                 "alg_flops_per_launch": work}
-        r["frac"] = (r["achieved"] / r["peak"]) if r["achieved"] else None
+                 "alg_flops_per_launch": work,
+                 "op_model": "SURVEY 8(d): 32 x 15 per sigma evaluation, 32 x 2 per distance evaluation"}
+        r["frac"] = (r["achieved"] / r["peak"]) if r["achieved"] and r["peak"] else None
         r["ms_per_launch"] = ms_k
         r["traffic"] = traffic.get(name)
         if r["traffic"] is not None:
@@ -469,7 +480,7 @@ def main():
 
         def copy_out(v, l):
             """vox_copy_level_async of level l into pinned host buffers; returns its bytes."""
-            n_l = int(v.view(l)["n"])
+            n_l = v.size(l)
             if l not in host or host[l]["key"].numel() < n_l:
                 host[l] = {"key": torch.empty(n_l, dtype=torch.int64).pin_memory(),
                            "mass": torch.empty(n_l, dtype=torch.float32).pin_memory(),

@@ -85,7 +85,7 @@ typedef struct {
     uint64_t cell_lo, cell_hi; /* this rank's top-cell range [lo, hi) */
     /* accumulated device milliseconds per stage since the last vox_stats_reset (profile=1) */
     double ms_bound, ms_emit, ms_sort, ms_reduce, ms_merge, ms_lod_scan, ms_lod, ms_total_vox, ms_total_lod;
-    double ms_lod_prep, ms_sggxh_quad, ms_sggxh_half, ms_sggxh_warp;   /* parts of ms_lod (n<=8, 9..16, >16) */
+    double ms_lod_prep, ms_sggxh_quad, ms_sggxh_half, ms_sggxh_warp;   /* parts of ms_lod: sums, SGGX-H n<=8, 9..16, >16 (hist mode: all in warp) */
     uint64_t launches;     /* kernels launched by the library since the last reset */
     /* SGGX-H algorithmic work since the last reset (profile=1): lobe sigma evaluations
      * (32 slices each), pair distance evaluations (32 slices each), parents with n > k */
@@ -130,12 +130,21 @@ vox_status vox_build_lod(vox_ctx* ctx, uint32_t levels);
 /* Highest level available for reading (0 after create). */
 vox_status vox_built_levels(vox_ctx* ctx, uint32_t* out);
 
-/* Borrowed view of a level (see vox_level_view). level > built -> VOX_ERR_LEVEL. */
+/* Number of voxels of a built level (no device work, no sync). level > built ->
+ * VOX_ERR_LEVEL; out NULL -> VOX_ERR_INVALID_ARG. */
+vox_status vox_level_size(vox_ctx* ctx, uint32_t level, uint64_t* out);
+
+/* Borrowed view of a level (see vox_level_view). level > built -> VOX_ERR_LEVEL. The build
+ * keeps only keys, the exact accumulators and lobe accumulators; the first read of a level
+ * allocates its fp32 views (mass, m6, cl: one rounding of each fixed-point sum, PREDICATES
+ * §8) and fills them on the ctx stream, so the view is valid once the stream reaches that
+ * point (vox_sync). Allocation failure -> VOX_ERR_OOM. */
 vox_status vox_read_level(vox_ctx* ctx, uint32_t level, vox_level_view* out);
 
 /* Copy a level into caller-owned buffers (device or host; any pointer may be NULL):
  * key [n], mass [n], m6 [n][6], ncl [n], cl [n][k][7]. Level 0 copies ncl = (mass > 0)
- * and cl = (mass, M) in slot 0. Synchronises the ctx stream when a buffer is host memory. */
+ * and cl = (mass, M) in slot 0. Forms the level's fp32 views first if needed (as
+ * vox_read_level). Synchronises the ctx stream. */
 vox_status vox_copy_level(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                           uint8_t* ncl, float* cl);
 
@@ -190,7 +199,8 @@ vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_
  * work enqueued on the ctx stream so far (an event), so the D2H of level l overlaps the
  * clustering of level l and the build of levels > l. Building further levels does not touch
  * lower levels; the caller synchronises `stream` before reading the buffers or destroying
- * the ctx.
+ * the ctx. The fp32 values are formed from the accumulators by a small kernel on `stream`
+ * into stream-ordered scratch (freed on `stream`; vox_trim releases it) before each D2H.
  * Level 0 supports key / mass / m6 only (ncl or cl non-NULL -> VOX_ERR_INVALID_ARG). */
 vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                                 uint8_t* ncl, float* cl, void* stream);

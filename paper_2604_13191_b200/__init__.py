@@ -76,6 +76,7 @@ def lib():
         getattr(L, name).argtypes = [vp, vp, vp, u64]
     L.vox_build_lod.argtypes = [vp, u32]
     L.vox_built_levels.argtypes = [vp, C.POINTER(u32)]
+    L.vox_level_size.argtypes = [vp, u32, C.POINTER(u64)]
     L.vox_read_level.argtypes = [vp, u32, C.POINTER(_View)]
     L.vox_copy_level.argtypes = [vp, u32, vp, vp, vp, vp, vp]
     L.vox_copy_level_acc.argtypes = [vp, u32, vp]
@@ -101,7 +102,7 @@ def lib():
     L.vox_last_error.argtypes = [vp]
     L.vox_destroy.argtypes = [vp]
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
-                 "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_read_level",
+                 "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_level_size", "vox_read_level",
                  "vox_copy_level", "vox_copy_level_acc", "vox_copy_level_async", "vox_encode_level", "vox_sample_splines",
                  "vox_sample_triangles", "vox_density_fibers", "vox_density_triangles", "vox_density_level", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):
@@ -257,6 +258,12 @@ class Vox:
         self._check(lib().vox_built_levels(self._h, C.byref(out)), "built_levels")
         return out.value
 
+    def size(self, level: int) -> int:
+        """vox_level_size: voxels of a built level (no device work)."""
+        out = C.c_uint64()
+        self._check(lib().vox_level_size(self._h, int(level), C.byref(out)), "level_size")
+        return out.value
+
     def view(self, level: int) -> dict:
         """Borrowed device pointers of a level (valid until the next mutating call)."""
         v = _View()
@@ -267,8 +274,7 @@ class Vox:
         """Copies of a level as torch tensors: key int64 [n], mass f32 [n], m6 f32 [n,6],
         ncl uint8 [n], cl f32 [n,k,7], acc int64 [n,7] (exact accumulators)."""
         import torch
-        v = self.view(level)
-        n = int(v["n"])
+        n = self.size(level)
         dev = torch.device(device)
         out = dict(key=torch.empty(n, dtype=torch.int64, device=dev),
                    mass=torch.empty(n, dtype=torch.float32, device=dev),
@@ -324,7 +330,7 @@ class Vox:
         """vox_density_level: occupancy [n] and axis densities [n,3] (YZ, XZ, XY) as cuda
         tensors, plus the 512-bit masks [n,8] (int64 bit patterns) when masks=True."""
         import torch
-        n = int(self.view(level)["n"])
+        n = self.size(level)
         out = {"occ": torch.empty(max(n, 1), dtype=torch.float32, device="cuda"),
                "axis": torch.empty((max(n, 1), 3), dtype=torch.float32, device="cuda")}
         if masks:
@@ -338,7 +344,7 @@ class Vox:
         (sggx6 uint8 [n,6]) and, optionally, of its lobes (cl6 uint8 [n,k,6]) and the jitter
         flags (uint8 [n]) as cuda tensors."""
         import torch
-        n = int(self.view(level)["n"])
+        n = self.size(level)
         out = {"sggx6": torch.empty((max(n, 1), 6), dtype=torch.uint8, device="cuda")}
         if lobes:
             out["cl6"] = torch.empty((max(n, 1), self.k, 6), dtype=torch.uint8, device="cuda")

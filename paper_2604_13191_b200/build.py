@@ -24,7 +24,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
-]
+] + os.environ.get("VOX_NVCC_EXTRA", "").split()   # experiment knobs (e.g. -DLV_MINB=5); empty by default
 
 
 def _stale(srcs, target):

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128, 1)
 k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
-             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
              const float* __restrict__ hu, int N, const uint32_t* __restrict__ gpg) {
     using SM = HistSmem<K>;
     constexpr int MAXN = SM::MAXN;
@@ -333,7 +333,6 @@ k_sggxh_hist(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (lane < 7) {
                 const long long a = lob[cc][lane];
                 pclacc[(p * K + slot) * 7 + lane] = a;
-                pcl[(p * K + slot) * 7 + lane] = deq32(a);
             }
             slot++;
         }
@@ -353,7 +352,7 @@ static cudaError_t launch_hist_k(vox_ctx* c, const uint32_t* list, const unsigne
     uint64_t nb = (P.n + SM::WARPS - 1) / SM::WARPS;
     nb = std::min<uint64_t>(std::max<uint64_t>(nb, 1), 148ull * 8);
     k_sggxh_hist<K><<<(unsigned)nb, SM::WARPS * 32, SM::total, c->stream>>>(
-        list, counts, C.acc, C.ncl, C.clacc, leaf, start, P.ncl, P.clacc, P.cl, c->d_hist_u, c->hist_n,
+        list, counts, C.acc, C.ncl, C.clacc, leaf, start, P.ncl, P.clacc, c->d_hist_u, c->hist_n,
         c->d_hist_pg);
     return cudaGetLastError();
 }

@@ -58,9 +58,8 @@ __device__ __forceinline__ int pair_t(int i, int j) { return j * (j - 1) / 2 + i
 template <int K>
 __global__ void k_lod_prep(const long long* __restrict__ cacc,
                            const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc, int leaf,
-                           const uint32_t* __restrict__ start, uint64_t V,
-                           long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
-                           uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+                           const uint32_t* __restrict__ start, uint64_t V, long long* __restrict__ pacc,
+                           uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
                            uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
     constexpr int MAXN = 8 * K;
     __shared__ unsigned s_hist[MAXN + 1];
@@ -82,39 +81,26 @@ __global__ void k_lod_prep(const long long* __restrict__ cacc,
         }
 #pragma unroll
         for (int e = 0; e < 7; e++) pacc[7 * p + e] = sum[e];
-        pmass[p] = deq32(sum[0]);
-#pragma unroll
-        for (int e = 0; e < 6; e++) pm6[6 * p + e] = deq32(sum[1 + e]);
         nlob[p] = (uint8_t)n;
         if (n <= K) {
             int slot = 0;
             for (uint32_t x = c0; x < c1; x++) {
                 if (leaf) {
                     if (cacc[7 * (uint64_t)x] > 0) {
-                        for (int e = 0; e < 7; e++) {
-                            const long long v = cacc[7 * (uint64_t)x + e];
-                            pclacc[(p * K + slot) * 7 + e] = v;
-                            pcl[(p * K + slot) * 7 + e] = deq32(v);
-                        }
+                        for (int e = 0; e < 7; e++) pclacc[(p * K + slot) * 7 + e] = cacc[7 * (uint64_t)x + e];
                         slot++;
                     }
                 } else {
                     for (int q = 0; q < cncl[x]; q++) {
                         const long long* src = cclacc + ((uint64_t)x * K + q) * 7;
                         if (src[0] == 0) continue;
-                        for (int e = 0; e < 7; e++) {
-                            pclacc[(p * K + slot) * 7 + e] = src[e];
-                            pcl[(p * K + slot) * 7 + e] = deq32(src[e]);
-                        }
+                        for (int e = 0; e < 7; e++) pclacc[(p * K + slot) * 7 + e] = src[e];
                         slot++;
                     }
                 }
             }
             for (int q = slot; q < K; q++)
-                for (int e = 0; e < 7; e++) {
-                    pclacc[(p * K + q) * 7 + e] = 0;
-                    pcl[(p * K + q) * 7 + e] = 0.0f;
-                }
+                for (int e = 0; e < 7; e++) pclacc[(p * K + q) * 7 + e] = 0;
             pncl[p] = (uint8_t)slot;
         } else {
             atomicAdd(&s_hist[n], 1u);
@@ -168,9 +154,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 template <int K>
 __global__ void __launch_bounds__(PREP_WARPS * 32)
 k_lod_prep_leaf(const long long* __restrict__ cacc,
-                const uint32_t* __restrict__ start, uint64_t V,
-                long long* __restrict__ pacc, float* __restrict__ pmass, float* __restrict__ pm6,
-                uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl,
+                const uint32_t* __restrict__ start, uint64_t V, long long* __restrict__ pacc,
+                uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
                 uint8_t* __restrict__ nlob, unsigned* __restrict__ hist) {
     constexpr int MAXN = 8 * K;
     extern __shared__ __align__(16) long long s_dyn[];   // per warp: 2 x rows | acc | lobes
@@ -264,19 +249,11 @@ k_lod_prep_leaf(const long long* __restrict__ cacc,
         }
         const unsigned hmask = __ballot_sync(0xffffffffu, hard);
         __syncwarp();
-        // coalesced write-back: accumulators, fp32 mass / m6, lobes of the final (n <= K) parents
-        for (int w = lane; w < np * 7; w += 32) {
-            const long long a = sacc[w];
-            pacc[7 * p0 + w] = a;
-            const int e = w % 7, pl = w / 7;
-            if (e == 0) pmass[p0 + pl] = deq32(a);
-            else pm6[6 * (p0 + pl) + e - 1] = deq32(a);
-        }
+        // coalesced write-back: accumulators, lobes of the final (n <= K) parents
+        for (int w = lane; w < np * 7; w += 32) pacc[7 * p0 + w] = sacc[w];
         for (int w = lane; w < np * K * 7; w += 32) {
             if ((hmask >> (w / (K * 7))) & 1u) continue;
-            const long long a = slob[w];
-            pclacc[(uint64_t)p0 * K * 7 + w] = a;
-            pcl[(uint64_t)p0 * K * 7 + w] = deq32(a);
+            pclacc[(uint64_t)p0 * K * 7 + w] = slob[w];
         }
         __syncwarp();
     }
@@ -410,7 +387,7 @@ __global__ void __launch_bounds__(QUAD_WARPS * 32)
 k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
-             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc, float* __restrict__ pcl) {
+             uint8_t* __restrict__ pncl, long long* __restrict__ pclacc) {
     __shared__ long long s_lobe[QUAD_WARPS][4][8][7];
     __shared__ __align__(16) float s_S[QUAD_WARPS][4][8][6];
     __shared__ float s_D[QUAD_WARPS][4][28];
@@ -600,18 +577,11 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             int slot = 0;
             for (int c = 0; c < n; c++) {
                 if (!((alive >> c) & 1u)) continue;
-                if (l < 7) {
-                    const long long v = lobe[c][l];
-                    pclacc[((uint64_t)p * K + slot) * 7 + l] = v;
-                    pcl[((uint64_t)p * K + slot) * 7 + l] = deq32(v);
-                }
+                if (l < 7) pclacc[((uint64_t)p * K + slot) * 7 + l] = lobe[c][l];
                 slot++;
             }
             for (int q = slot; q < K; q++)
-                if (l < 7) {
-                    pclacc[((uint64_t)p * K + q) * 7 + l] = 0;
-                    pcl[((uint64_t)p * K + q) * 7 + l] = 0.0f;
-                }
+                if (l < 7) pclacc[((uint64_t)p * K + q) * 7 + l] = 0;
             if (l == 0) pncl[p] = (uint8_t)slot;
         }
         __syncwarp();
@@ -678,8 +648,7 @@ template <int K>
 __global__ void __launch_bounds__(LOD_WARPS * 32)
 k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc,
-             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
-             float* __restrict__ pcl) {
+             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc) {
     using SM = LodSmem<K>;
     constexpr int MAXP = SM::MAXP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -774,11 +743,7 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         int slot = 0;
         for (int cc = 0; cc < n; cc++) {
             if (!((alive >> cc) & 1ull)) continue;
-            if (lane < 7) {
-                const long long a = list_[cc][lane];
-                pclacc[(p * K + slot) * 7 + lane] = a;
-                pcl[(p * K + slot) * 7 + lane] = deq32(a);
-            }
+            if (lane < 7) pclacc[(p * K + slot) * 7 + lane] = list_[cc][lane];
             slot++;
         }
         if (lane == 0) pncl[p] = (uint8_t)slot;
@@ -804,8 +769,7 @@ template <int K>
 __global__ void __launch_bounds__(HALF_WARPS * 32)
 k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const uint8_t* __restrict__ cncl, const long long* __restrict__ cclacc,
-             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc,
-             float* __restrict__ pcl) {
+             const uint32_t* __restrict__ start, uint8_t* __restrict__ pncl, long long* __restrict__ pclacc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t* ptab = reinterpret_cast<uint16_t*>(smem_raw);   // t -> (i << 8) | j, 120 entries
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -937,11 +901,7 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             int slot = 0;
             for (int cc = 0; cc < n; cc++) {
                 if (!((alive >> cc) & 1u)) continue;
-                if (l < 7) {
-                    const long long a = H.lobe[cc][l];
-                    pclacc[(p * K + slot) * 7 + l] = a;
-                    pcl[(p * K + slot) * 7 + l] = deq32(a);
-                }
+                if (l < 7) pclacc[(p * K + slot) * 7 + l] = H.lobe[cc][l];
                 slot++;
             }
             if (l == 0) pncl[p] = (uint8_t)slot;
@@ -950,17 +910,25 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     }
 }
 
+// fp32 views from the exact accumulators (§8: one rounding of the fixed-point sum): a word per
+// thread, grid-stride, so every array is read and written coalesced. Lobes past ncl are 0.
 __global__ void k_finalize(uint64_t n, const long long* __restrict__ acc, float* __restrict__ mass,
                            float* __restrict__ m6, const uint8_t* __restrict__ ncl, const long long* __restrict__ clacc,
                            float* __restrict__ cl, int K) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        mass[v] = deq32(acc[7 * v]);
-        for (int e = 0; e < 6; e++) m6[6 * v + e] = deq32(acc[7 * v + 1 + e]);
-        if (cl) {
-            const int m = ncl[v];
-            for (int q = 0; q < K; q++)
-                for (int e = 0; e < 7; e++)
-                    cl[(v * K + q) * 7 + e] = q < m ? deq32(clacc[(v * K + q) * 7 + e]) : 0.0f;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (mass)
+        for (uint64_t v = t0; v < n; v += stride) mass[v] = deq32(acc[7 * v]);
+    if (m6)
+        for (uint64_t w = t0; w < 6 * n; w += stride) {
+            const uint64_t v = w / 6;
+            m6[w] = deq32(acc[7 * v + 1 + (w - 6 * v)]);
+        }
+    if (cl) {
+        const uint64_t per = 7ull * K;
+        for (uint64_t w = t0; w < per * n; w += stride) {
+            const uint64_t v = w / per;
+            const int q = (int)((w - per * v) / 7);
+            cl[w] = q < ncl[v] ? deq32(clacc[w]) : 0.0f;
         }
     }
 }
@@ -972,14 +940,14 @@ static unsigned grid_for(uint64_t n, int threads = 256) {
     return (unsigned)b;
 }
 
-cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters) {
-    if (L.n == 0) return cudaSuccess;
-    k_finalize<<<grid_for(L.n), 256, 0, c->stream>>>(L.n, L.acc, L.mass, L.m6, clusters ? L.ncl : nullptr,
-                                                     clusters ? L.clacc : nullptr, clusters ? L.cl : nullptr,
-                                                     (int)c->K);
+cudaError_t launch_finalize(vox_ctx* c, cudaStream_t s, uint64_t n, const long long* acc, const uint8_t* ncl,
+                            const long long* clacc, float* mass, float* m6, float* cl) {
+    if (n == 0 || (!mass && !m6 && !cl)) return cudaSuccess;
+    k_finalize<<<grid_for(6 * n), 256, 0, s>>>(n, acc, mass, m6, ncl, clacc, cl, (int)c->K);
     c->st.launches++;
     return cudaGetLastError();
 }
+
 
 #define CK(x)                                                          \
     do {                                                               \
@@ -989,6 +957,17 @@ cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters) {
             return e_ == cudaErrorMemoryAllocation ? VOX_ERR_OOM : VOX_ERR_CUDA; \
         }                                                              \
     } while (0)
+
+vox_status ensure_f32(vox_ctx* c, int level) {
+    Level& L = c->lv[level];
+    if (L.f32 || L.n == 0) return VOX_OK;
+    CK(dalloc(c, (void**)&L.mass, L.n * 4));
+    CK(dalloc(c, (void**)&L.m6, L.n * 24));
+    if (level > 0) CK(dalloc(c, (void**)&L.cl, L.n * c->K * 28));
+    CK(launch_finalize(c, c->stream, L.n, L.acc, L.ncl, L.clacc, L.mass, L.m6, level > 0 ? L.cl : nullptr));
+    L.f32 = true;
+    return VOX_OK;
+}
 
 template <int K>
 static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t* start, Level& P) {
@@ -1009,12 +988,11 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 3);
         const size_t psm = (size_t)PREP_WARPS * (PREP_WARP_WORDS + PREP_PAR * K * 7) * sizeof(long long);
         CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-        k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.acc, start, V, P.acc,
-                                                                            P.mass, P.m6, P.ncl, P.clacc, P.cl,
-                                                                            nlob, hist);
+        k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.acc, start, V, P.acc, P.ncl,
+                                                                            P.clacc, nlob, hist);
     } else {
-        k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.acc, C.ncl, C.clacc, leaf, start, V,
-                                                         P.acc, P.mass, P.m6, P.ncl, P.clacc, P.cl, nlob, hist);
+        k_lod_prep<K><<<grid_for(V), 256, 0, c->stream>>>(C.acc, C.ncl, C.clacc, leaf, start, V, P.acc, P.ncl,
+                                                         P.clacc, nlob, hist);
     }
     timer_end(c, c->t_prep);
     // key, mass and m6 of the level are final here (SGGX-H only writes lobes): an event lets
@@ -1041,7 +1019,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         qb = std::min<uint64_t>(std::max<uint64_t>(qb, 1), 148ull * 48);
         timer_begin(c, c->t_quad);
         k_sggxh_quad<K><<<(unsigned)qb, QUAD_WARPS * 32, 0, c->stream>>>(list, counts, C.acc, C.ncl, C.clacc, leaf,
-                                                                        start, P.ncl, P.clacc, P.cl);
+                                                                        start, P.ncl, P.clacc);
         timer_end(c, c->t_quad);
         c->st.launches++;
     }
@@ -1052,7 +1030,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         hb = std::min<uint64_t>(std::max<uint64_t>(hb, 1), 148ull * 32);
         timer_begin(c, c->t_half);
         k_sggxh_half<K><<<(unsigned)hb, HALF_WARPS * 32, smem, c->stream>>>(list, counts, C.ncl, C.clacc, start,
-                                                                           P.ncl, P.clacc, P.cl);
+                                                                           P.ncl, P.clacc);
         timer_end(c, c->t_half);
         c->st.launches++;
     }
@@ -1063,7 +1041,7 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
         wb = std::min<uint64_t>(std::max<uint64_t>(wb, 1), 148ull * 32);
         timer_begin(c, c->t_warp);
         k_sggxh_warp<K><<<(unsigned)wb, LOD_WARPS * 32, smem, c->stream>>>(list, counts, C.ncl, C.clacc, start,
-                                                                          P.ncl, P.clacc, P.cl);
+                                                                          P.ncl, P.clacc);
         timer_end(c, c->t_warp);
         c->st.launches++;
     }
@@ -1163,11 +1141,8 @@ vox_status build_level(vox_ctx* c, int l) {
     timer_end(c, c->t_lodscan);
     P.n = V;
     CK(dalloc(c, (void**)&P.acc, (uint64_t)V * 56));
-    CK(dalloc(c, (void**)&P.mass, (uint64_t)V * 4));
-    CK(dalloc(c, (void**)&P.m6, (uint64_t)V * 24));
     CK(dalloc(c, (void**)&P.ncl, (uint64_t)V));
     CK(dalloc(c, (void**)&P.clacc, (uint64_t)V * K * 56));
-    CK(dalloc(c, (void**)&P.cl, (uint64_t)V * K * 28));
     timer_begin(c, c->t_lod);
     const int leaf = (l == 1);
     vox_status s;
@@ -1239,11 +1214,8 @@ vox_status unpack_level(vox_ctx* c, int level, const void* buf, uint64_t n) {
     if (n == 0) return VOX_OK;
     CK(dalloc(c, (void**)&L.key, n * 8));
     CK(dalloc(c, (void**)&L.acc, n * 56));
-    CK(dalloc(c, (void**)&L.mass, n * 4));
-    CK(dalloc(c, (void**)&L.m6, n * 24));
     CK(dalloc(c, (void**)&L.ncl, n));
     CK(dalloc(c, (void**)&L.clacc, n * K * 56));
-    CK(dalloc(c, (void**)&L.cl, n * K * 28));
     CK(cudaMemsetAsync(c->d_flags, 0, 4, c->stream));
     k_unpack<<<grid_for(n), 256, 0, c->stream>>>(n, (const long long*)buf, (int)K, L.key, L.acc, L.ncl, L.clacc,
                                                  c->d_flags);
@@ -1255,7 +1227,6 @@ vox_status unpack_level(vox_ctx* c, int level, const void* buf, uint64_t n) {
         free_level(c, L);
         return VOX_ERR_COMM;
     }
-    CK(launch_finalize(c, L, true));
     return VOX_OK;
 }
 

@@ -92,13 +92,11 @@ static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32
     return VOX_OK;
 }
 
-vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6, uint64_t V) {
+vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t V) {
     Level& L0 = c->lv[0];
     if (V == 0) {
         dfree(c, nkey);
         dfree(c, nacc);
-        dfree(c, nmass);
-        dfree(c, nm6);
         return VOX_OK;
     }
     if (L0.n > 0) {
@@ -112,20 +110,12 @@ vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* n
             M.n = tot;
             CK(dalloc(c, (void**)&M.key, tot * 8));
             CK(dalloc(c, (void**)&M.acc, tot * 56));
-            CK(dalloc(c, (void**)&M.mass, tot * 4));
-            CK(dalloc(c, (void**)&M.m6, tot * 24));
             CK(cudaMemcpyAsync(M.key, L0.key, L0.n * 8, cudaMemcpyDeviceToDevice, c->stream));
             CK(cudaMemcpyAsync(M.key + L0.n, nkey, V * 8, cudaMemcpyDeviceToDevice, c->stream));
             CK(cudaMemcpyAsync(M.acc, L0.acc, L0.n * 56, cudaMemcpyDeviceToDevice, c->stream));
             CK(cudaMemcpyAsync(M.acc + 7 * L0.n, nacc, V * 56, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(M.mass, L0.mass, L0.n * 4, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(M.mass + L0.n, nmass, V * 4, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(M.m6, L0.m6, L0.n * 24, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(M.m6 + 6 * L0.n, nm6, V * 24, cudaMemcpyDeviceToDevice, c->stream));
             dfree(c, nkey);
             dfree(c, nacc);
-            dfree(c, nmass);
-            dfree(c, nm6);
             free_level(c, L0);
             L0 = M;
             timer_end(c, c->t_merge);
@@ -137,8 +127,6 @@ vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* n
         L0.n = V;
         L0.key = nkey;
         L0.acc = nacc;
-        L0.mass = nmass;
-        L0.m6 = nm6;
         return VOX_OK;
     } else {
         timer_begin(c, c->t_merge);
@@ -177,17 +165,12 @@ vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* n
         dfree(c, k0); dfree(c, k1); dfree(c, i0); dfree(c, i1);
         dfree(c, nkey);
         dfree(c, nacc);
-        dfree(c, nmass);
-        dfree(c, nm6);
         free_level(c, L0);
         L0.n = VM;
         L0.key = mkey;
         L0.acc = macc;
         timer_end(c, c->t_merge);
     }
-    CK(dalloc(c, (void**)&L0.mass, (L0.n ? L0.n : 1) * 4));
-    CK(dalloc(c, (void**)&L0.m6, (L0.n ? L0.n : 1) * 24));
-    CK(launch_finalize(c, L0, false));
     return VOX_OK;
 }
 
@@ -307,14 +290,12 @@ __device__ __forceinline__ unsigned key_rank(const unsigned* bm, const unsigned*
 }
 
 // one voxel's exact sums over its pairs (§5, §7, §8), written as a key-ordered output row
+// (the fp32 views are produced on demand from the accumulators, launch_finalize)
 __device__ __forceinline__ void emit_voxel(uint64_t key, const long long (&a)[7], uint64_t r, uint64_t* okey,
-                                          long long* oacc, float* omass, float* om6) {
+                                          long long* oacc) {
     okey[r] = key;
 #pragma unroll
     for (int e = 0; e < 7; e++) oacc[7 * r + e] = a[e];
-    omass[r] = deq32(a[0]);
-#pragma unroll
-    for (int e = 0; e < 6; e++) om6[6 * r + e] = deq32(a[1 + e]);
 }
 
 __device__ __forceinline__ void add_pair(uint64_t val, const float4* __restrict__ ptab, long long (&a)[7]) {
@@ -339,7 +320,7 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
              const unsigned long long* __restrict__ off, const unsigned* __restrict__ cnt,
              const unsigned* __restrict__ alist, const unsigned* __restrict__ nact,
              const unsigned* __restrict__ voff, int lbits, uint64_t* __restrict__ okey,
-             long long* __restrict__ oacc, float* __restrict__ omass, float* __restrict__ om6) {
+             long long* __restrict__ oacc) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
     unsigned* bm = reinterpret_cast<unsigned*>(s_raw);                      // [words]
@@ -406,7 +387,7 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
                 const unsigned p0 = r == 0 ? 0u : cur[r - 1], p1 = cur[r];
                 long long a[7] = {0, 0, 0, 0, 0, 0, 0};
                 for (unsigned p = p0; p < p1; p++) add_pair(vals[o + sidx[p]], ptab, a);
-                emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc, omass, om6);
+                emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc);
             }
             __syncthreads();
         } else {
@@ -438,7 +419,7 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
                     long long a[7];
 #pragma unroll
                     for (int e = 0; e < 7; e++) a[e] = (long long)acc[7 * x + e];
-                    emit_voxel(kbase | lkey[x], a, (uint64_t)vb + r0 + x, okey, oacc, omass, om6);
+                    emit_voxel(kbase | lkey[x], a, (uint64_t)vb + r0 + x, okey, oacc);
                 }
                 __syncthreads();
             }
@@ -459,7 +440,7 @@ k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
                   const unsigned* __restrict__ cnt, const unsigned* __restrict__ alist,
                   const unsigned* __restrict__ nact, const unsigned* __restrict__ voff, int lbits,
                   unsigned* __restrict__ big, unsigned* __restrict__ nbig, uint64_t* __restrict__ okey,
-                  long long* __restrict__ oacc, float* __restrict__ omass, float* __restrict__ om6) {
+                  long long* __restrict__ oacc) {
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -537,7 +518,7 @@ k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
             const unsigned p0 = r == 0 ? 0u : cur[r - 1], p1 = cur[r];
             long long a[7] = {0, 0, 0, 0, 0, 0, 0};
             for (unsigned p = p0; p < p1; p++) add_pair(vals[o + sidx[p]], ptab, a);
-            emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc, omass, om6);
+            emit_voxel(keys[o + sidx[p0]], a, (uint64_t)vb + r, okey, oacc);
         }
         __syncwarp();
     }
@@ -616,11 +597,8 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     timer_begin(c, c->t_reduce);
     uint64_t* nkey = nullptr;
     long long* nacc = nullptr;
-    float *nmass = nullptr, *nm6 = nullptr;
     CK(dalloc(c, (void**)&nkey, (uint64_t)V * 8));
     CK(dalloc(c, (void**)&nacc, (uint64_t)V * 56));
-    CK(dalloc(c, (void**)&nmass, (uint64_t)V * 4));
-    CK(dalloc(c, (void**)&nm6, (uint64_t)V * 24));
     // small bins: warp per bin; the others (listed by it) then get a block each
     unsigned* big = nullptr;
     CK(dalloc(c, (void**)&big, nb * 4 + 4));
@@ -630,12 +608,12 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     CK(cudaFuncSetAttribute(k_bin_reduce_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
     const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + WB_WARPS - 1) / WB_WARPS, 148ull * 32);
     k_bin_reduce_warp<<<wgrid, WB_WARPS * 32, wsm, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact,
-                                                                voff, lbits, big, nbig, nkey, nacc, nmass, nm6);
+                                                                voff, lbits, big, nbig, nkey, nacc);
     const size_t smem = 2 * (size_t)words * 4 + (BIN_VMAX + 1) * 4 + BIN_NMAX * 2 + 16;
     static_assert(BIN_CHUNK * 7 * 8 + BIN_CHUNK * 2 <= (BIN_VMAX + 1) * 4 + BIN_NMAX * 2, "fallback must fit");
     CK(cudaFuncSetAttribute(k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_bin_reduce<<<grid, BIN_THREADS, smem, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, big, nbig, voff,
-                                                         lbits, nkey, nacc, nmass, nm6);
+                                                         lbits, nkey, nacc);
     c->st.launches += 2;
     CK(cudaGetLastError());
     timer_end(c, c->t_reduce);
@@ -647,8 +625,6 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     dfree(c, big);
     out.key = nkey;
     out.acc = nacc;
-    out.mass = nmass;
-    out.m6 = nm6;
     out.n = V;
     return VOX_OK;
 }

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <chrono>
 #include <map>
+#include <set>
 #include <unordered_map>
 #include <mutex>
 #include <new>
@@ -40,36 +41,40 @@ static size_t round_bytes(size_t b) {
     return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);   // 2 MiB granularity
 }
 
-cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
+cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) { return dalloc_s(c, c->stream, p, bytes); }
+
+// allocation ordered on stream s (the block cache is keyed by stream: a freed block is only
+// handed out again on the stream that used it)
+cudaError_t dalloc_s(vox_ctx* c, cudaStream_t s, void** p, size_t bytes) {
     *p = nullptr;
     const size_t want = round_bytes((bytes ? bytes : 16) + 64);   // >= 64 B slack (bulk-copy tails)
     const auto t0 = std::chrono::steady_clock::now();
     {
         std::lock_guard<std::mutex> lk(g_mem_mu);
-        auto it = g_free.lower_bound({c->stream, want});
-        if (it != g_free.end() && it->first.first == c->stream && it->first.second <= 2 * want) {
+        auto it = g_free.lower_bound({s, want});
+        if (it != g_free.end() && it->first.first == s && it->first.second <= 2 * want) {
             *p = it->second;
-            g_live[*p] = CachedBlock{c->stream, it->first.second};
+            g_live[*p] = CachedBlock{s, it->first.second};
             g_free.erase(it);
         }
     }
     cudaError_t e = cudaSuccess;
     if (!*p) {
-        e = cudaMallocAsync(p, want, c->stream);
+        e = cudaMallocAsync(p, want, s);
         if (e == cudaErrorMemoryAllocation) {
             // release the cached blocks of this stream, return the pool's unused memory, retry
             cudaGetLastError();
-            vox_trim_stream(c->stream);
-            cudaStreamSynchronize(c->stream);
+            vox_trim_stream(s);
+            cudaStreamSynchronize(s);
             int dev = 0;
             cudaMemPool_t pool;
             if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
                 cudaMemPoolTrimTo(pool, 0);
-            e = cudaMallocAsync(p, want, c->stream);
+            e = cudaMallocAsync(p, want, s);
         }
         if (e == cudaSuccess) {
             std::lock_guard<std::mutex> lk(g_mem_mu);
-            g_live[*p] = CachedBlock{c->stream, want};
+            g_live[*p] = CachedBlock{s, want};
         }
     }
     c->st.host_ms_alloc += host_ms_since(t0);
@@ -175,8 +180,8 @@ void free_level(vox_ctx* c, Level& L) {
             c->ev_read_pending[l] = false;
         }
     }
-    dfree(c, L.key); dfree(c, L.acc); dfree(c, L.mass); dfree(c, L.m6);
-    dfree(c, L.ncl); dfree(c, L.clacc); dfree(c, L.cl);
+    dfree(c, L.key); dfree(c, L.acc); dfree(c, L.ncl); dfree(c, L.clacc);
+    dfree(c, L.mass); dfree(c, L.m6); dfree(c, L.cl);
     L = Level();
 }
 
@@ -523,7 +528,7 @@ static vox_status voxelize_common(vox_ctx* c, const float* a, const float* b, ui
             c->err = "internal: pair capacity overflow";
             return VOX_ERR_CUDA;
         }
-        return merge_into_leaf(c, leaf.key, leaf.acc, leaf.mass, leaf.m6, leaf.n);
+        return merge_into_leaf(c, leaf.key, leaf.acc, leaf.n);
     };
     vox_status res = VOX_OK;
     for (size_t part = 0; part + 1 < cuts.size() && res == VOX_OK; part++) {
@@ -711,9 +716,18 @@ vox_status vox_built_levels(vox_ctx* c, uint32_t* out) {
     return VOX_OK;
 }
 
+vox_status vox_level_size(vox_ctx* c, uint32_t level, uint64_t* out) {
+    if (!c || !out) return VOX_ERR_INVALID_ARG;
+    if ((int)level > c->built) return VOX_ERR_LEVEL;
+    *out = c->lv[level].n;
+    return VOX_OK;
+}
+
 vox_status vox_read_level(vox_ctx* c, uint32_t level, vox_level_view* out) {
     if (!c || !out) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
+    vox_status s = ensure_f32(c, (int)level);   // the build keeps only the exact accumulators
+    if (s != VOX_OK) return s;
     const Level& L = c->lv[level];
     out->n = L.n;
     out->key = L.key;
@@ -725,15 +739,15 @@ vox_status vox_read_level(vox_ctx* c, uint32_t level, vox_level_view* out) {
     return VOX_OK;
 }
 
-__global__ void k_leaf_lobes(uint64_t n, const float* __restrict__ mass, const float* __restrict__ m6, int K,
-                             uint8_t* __restrict__ ncl, float* __restrict__ cl) {
+// a leaf's single lobe is (mass, M) iff mass > 0 (D17)
+__global__ void k_leaf_lobes(uint64_t n, const long long* __restrict__ acc, int K, uint8_t* __restrict__ ncl,
+                             float* __restrict__ cl) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        const bool has = mass[v] > 0.0f;
+        const bool has = acc[7 * v] > 0;
         if (ncl) ncl[v] = has ? 1 : 0;
         if (cl) {
             for (int q = 0; q < K; q++)
-                for (int e = 0; e < 7; e++)
-                    cl[(v * K + q) * 7 + e] = (q == 0 && has) ? (e == 0 ? mass[v] : m6[6 * v + e - 1]) : 0.0f;
+                for (int e = 0; e < 7; e++) cl[(v * K + q) * 7 + e] = (q == 0 && has) ? deq32(acc[7 * v + e]) : 0.0f;
         }
     }
 }
@@ -831,6 +845,10 @@ vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass
     const uint64_t n = L.n;
     const uint32_t K = c->K;
     if (n == 0) return VOX_OK;
+    if (mass || m6 || (level > 0 && cl)) {
+        vox_status s = ensure_f32(c, (int)level);
+        if (s != VOX_OK) return s;
+    }
     if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, c->stream));
     if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, c->stream));
     if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, c->stream));
@@ -843,7 +861,7 @@ vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass
         if (ncl) CKS(dalloc(c, (void**)&dn, n));
         if (cl) CKS(dalloc(c, (void**)&dc, n * K * 28));
         uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 32);
-        k_leaf_lobes<<<(unsigned)blocks, 256, 0, c->stream>>>(n, L.mass, L.m6, (int)K, dn, dc);
+        k_leaf_lobes<<<(unsigned)blocks, 256, 0, c->stream>>>(n, L.acc, (int)K, dn, dc);
         c->st.launches++;
         if (ncl) CKS(cudaMemcpyAsync(ncl, dn, n, cudaMemcpyDefault, c->stream));
         if (cl) CKS(cudaMemcpyAsync(cl, dc, n * K * 28, cudaMemcpyDefault, c->stream));
@@ -873,16 +891,40 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
         CKS(cudaStreamWaitEvent(s, e0, 0));
         CKS(cudaEventDestroy(e0));
     }
+    // the fp32 views are formed from the accumulators on `s` into stream-ordered scratch
+    // (unless the level already holds them), so the build on the ctx stream is not delayed
+    const bool have = L.f32;
     if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, s));
-    if (mass) CKS(cudaMemcpyAsync(mass, L.mass, n * 4, cudaMemcpyDefault, s));
-    if (m6) CKS(cudaMemcpyAsync(m6, L.m6, n * 24, cudaMemcpyDefault, s));
+    if (mass || m6) {
+        float *tm = have ? L.mass : nullptr, *t6 = have ? L.m6 : nullptr;
+        if (!have) {
+            if (mass) CKS(dalloc_s(c, s, (void**)&tm, n * 4));
+            if (m6) CKS(dalloc_s(c, s, (void**)&t6, n * 24));
+            CKS(launch_finalize(c, s, n, L.acc, nullptr, nullptr, mass ? tm : nullptr, m6 ? t6 : nullptr, nullptr));
+        }
+        if (mass) CKS(cudaMemcpyAsync(mass, tm, n * 4, cudaMemcpyDefault, s));
+        if (m6) CKS(cudaMemcpyAsync(m6, t6, n * 24, cudaMemcpyDefault, s));
+        if (!have) {
+            dfree(c, tm);
+            dfree(c, t6);
+        }
+    }
     cudaEvent_t ev;
     CKS(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CKS(cudaEventRecord(ev, c->stream));      // after everything that produced the level
     CKS(cudaStreamWaitEvent(s, ev, 0));
     CKS(cudaEventDestroy(ev));
     if (ncl) CKS(cudaMemcpyAsync(ncl, L.ncl, n, cudaMemcpyDefault, s));
-    if (cl) CKS(cudaMemcpyAsync(cl, L.cl, n * c->K * 28, cudaMemcpyDefault, s));
+    if (cl) {
+        float* tc = have ? L.cl : nullptr;
+        if (!have) {
+            CKS(dalloc_s(c, s, (void**)&tc, n * c->K * 28));
+            CKS(launch_finalize(c, s, n, nullptr, L.ncl, L.clacc, nullptr, nullptr, tc));
+        }
+        CKS(cudaMemcpyAsync(cl, tc, n * c->K * 28, cudaMemcpyDefault, s));
+        if (!have) dfree(c, tc);
+    }
+    if (s != c->stream) c->aux_streams.insert(s);
     // the level's arrays are being read on `s` until here: free_level / import wait on it
     if (!c->ev_read[level]) CKS(cudaEventCreateWithFlags(&c->ev_read[level], cudaEventDisableTiming));
     CKS(cudaEventRecord(c->ev_read[level], s));
@@ -1007,6 +1049,11 @@ vox_status vox_trim(vox_ctx* c) {
     if (!c) return VOX_ERR_INVALID_ARG;
     CKS(ssync(c));
     vox_trim_stream(c->stream);
+    for (cudaStream_t s : c->aux_streams) {   // scratch of async copies, cached per stream
+        CKS(cudaStreamSynchronize(s));
+        vox_trim_stream(s);
+        CKS(cudaStreamSynchronize(s));
+    }
     CKS(ssync(c));
     return VOX_OK;
 }

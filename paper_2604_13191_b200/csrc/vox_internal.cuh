@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <initializer_list>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -146,15 +147,19 @@ __device__ __forceinline__ long long find_key(const uint64_t* __restrict__ keys,
 
 // ---------------------------------------------------------------- host-side state
 
+// A level as the build leaves it: keys, exact accumulators and (levels >= 1) lobes. The fp32
+// views (mass, m6, cl) are not written by the build; they are produced from the accumulators
+// on demand (ensure_f32 / launch_finalize) when a caller reads the level.
 struct Level {
     uint64_t n = 0;
     uint64_t* key = nullptr;
     long long* acc = nullptr;   // [n][7]
-    float* mass = nullptr;      // [n]
-    float* m6 = nullptr;        // [n][6]
     uint8_t* ncl = nullptr;     // [n]       (levels >= 1)
     long long* clacc = nullptr; // [n][K][7] (levels >= 1)
-    float* cl = nullptr;        // [n][K][7] (levels >= 1)
+    float* mass = nullptr;      // [n]        fp32 view, valid iff f32
+    float* m6 = nullptr;        // [n][6]     fp32 view, valid iff f32
+    float* cl = nullptr;        // [n][K][7]  fp32 view (levels >= 1), valid iff f32
+    bool f32 = false;
 };
 
 enum CtxState { ST_CREATED = 0, ST_VOXELIZED = 1, ST_LOD = 2 };
@@ -199,6 +204,7 @@ struct vox_ctx {
     cudaEvent_t ev_read[VOX_MAX_LEVELS] = {};
     bool ev_read_pending[VOX_MAX_LEVELS] = {};
     int dev = 0;                            // device of the ctx (event pool key)
+    std::set<cudaStream_t> aux_streams;     // caller streams that received async-copy scratch
     void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
     void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
@@ -215,6 +221,7 @@ namespace vox {
 
 // allocation helpers (stream-ordered)
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes);
+cudaError_t dalloc_s(vox_ctx* c, cudaStream_t s, void** p, size_t bytes);   // ordered on stream s
 cudaError_t ssync(vox_ctx* c);   // cudaStreamSynchronize with host-time accounting
 struct ReadItem {
     void* dst;
@@ -245,14 +252,12 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
 struct LeafSet {
     uint64_t* key = nullptr;
     long long* acc = nullptr;
-    float* mass = nullptr;
-    float* m6 = nullptr;
     uint64_t n = 0;
 };
 vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, Bins bins, uint64_t nb,
                        const float4* ptab, LeafSet& out);
 // merges a new leaf set into lv[0] (concatenation when its keys follow, exact sums otherwise)
-vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, float* nmass, float* nm6, uint64_t V);
+vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t V);
 // per-call helpers (k_reduce.cu)
 vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT);
 vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigned long long** off_out,
@@ -283,8 +288,12 @@ cudaError_t launch_encode(vox_ctx* c, const Level& L, int leaf, uint8_t* out6, u
 cudaError_t launch_sggxh_hist(vox_ctx* c, int K, const uint32_t* list, const unsigned* counts, const Level& C,
                               int leaf, const uint32_t* start, Level& P);
 void host_theta(float theta[32][3], float coef[32][6]);
-// fp32 outputs of a level from its accumulators (k_lod.cu)
-cudaError_t launch_finalize(vox_ctx* c, Level& L, bool clusters);
+// fp32 views of a level from its accumulators (k_lod.cu): writes whichever of mass / m6 / cl
+// is non-null, for n records, on stream s
+cudaError_t launch_finalize(vox_ctx* c, cudaStream_t s, uint64_t n, const long long* acc, const uint8_t* ncl,
+                            const long long* clacc, float* mass, float* m6, float* cl);
+// allocates and fills the level's fp32 views once (ctx stream); no-op when already valid
+vox_status ensure_f32(vox_ctx* c, int level);
 // multi-GPU records (k_lod.cu)
 uint64_t record_bytes(uint32_t K);
 cudaError_t launch_pack(vox_ctx* c, int level, void* buf);

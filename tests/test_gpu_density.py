@@ -110,7 +110,7 @@ def test_density_states(P):
     v.voxelize_fibers(S, R)
     v.density_fibers(S, R)
     v.build_lod(2)
-    assert v.density_level(2)["occ"].numel() == v.view(2)["n"]
+    assert v.density_level(2)["occ"].numel() == v.size(2)
 
 
 @pytest.mark.parametrize("seed", [0, 1])

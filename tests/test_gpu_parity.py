@@ -144,9 +144,14 @@ def test_host_entry_points(P):
     w.voxelize_triangles_host(c["tris"])
     side = torch.cuda.Stream()
     outs = {}
+    n0 = w.size(0)   # the leaf level: fp32 views formed on the side stream from the accumulators
+    outs[0] = {"key": torch.empty(n0, dtype=torch.int64).pin_memory(),
+               "mass": torch.empty(n0, dtype=torch.float32).pin_memory(),
+               "m6": torch.empty((n0, 6), dtype=torch.float32).pin_memory()}
+    w.copy_level_async(0, outs[0], side)
     for l in range(1, 7):
         w.build_lod(l)
-        n = int(w.view(l)["n"])
+        n = w.size(l)
         outs[l] = {"key": torch.empty(n, dtype=torch.int64).pin_memory(),
                    "mass": torch.empty(n, dtype=torch.float32).pin_memory(),
                    "m6": torch.empty((n, 6), dtype=torch.float32).pin_memory(),
@@ -154,6 +159,14 @@ def test_host_entry_points(P):
                    "cl": torch.empty((n, 3, 7), dtype=torch.float32).pin_memory()}
         w.copy_level_async(l, outs[l], side)
     side.synchronize()
+    r = o.level(0)
+    assert np.array_equal(outs[0]["key"].numpy().astype(np.uint64), r["key"])
+    assert np.array_equal(outs[0]["mass"].numpy(), r["mass"]) and np.array_equal(outs[0]["m6"].numpy(), r["m6"])
+    # borrowed views: the first read forms the level's fp32 arrays on the ctx stream, later
+    # copies read those arrays
+    for l in (0, 3):
+        assert int(w.view(l)["n"]) == w.size(l)
+        _cmp_level(w.level(l, device="cpu"), o.level(l), l, "view")
     for l in range(1, 7):
         r = o.level(l)
         assert np.array_equal(outs[l]["key"].numpy().astype(np.uint64), r["key"])
@@ -279,7 +292,7 @@ def test_edge_cases_new_entry_points(P):
     v.sample_splines(torch.tensor([[[5.0, 5, 5], [6, 6, 6], [7, 7, 7], [8, 8, 8]]], device="cuda"),
                      torch.tensor([0.1], device="cuda"), 4)
     v.build_lod(4)
-    assert all(int(v.view(l)["n"]) == 0 for l in range(5))
+    assert all(v.size(l) == 0 for l in range(5))
     assert v.encode_level(2)["sggx6"].numel() == 0
     v.density_fibers(far, torch.tensor([0.1], device="cuda"))
     assert v.density_level(3)["occ"].numel() == 0

@@ -56,7 +56,7 @@ def nhist():
         n = torch.zeros(len(cur["key"]), dtype=torch.long, device="cuda").index_add_(0, idx, lob)
         h = torch.bincount(n[n > v.k], minlength=25).cpu().tolist()
         print(l, "parents", len(n), "hard", int((n > v.k).sum()),
-              {k: round(st[k], 2) for k in ("ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_half", "ms_sggxh_warp")},
+              {k: round(st[k], 2) for k in ("ms_lod_scan", "ms_lod_prep", "ms_sggxh_quad", "ms_sggxh_half", "ms_sggxh_warp")},
               {k: x for k, x in enumerate(h) if x}, flush=True)
         prev = cur
 
