@@ -6,8 +6,6 @@
 // so no re-sort). One warp per parent: lanes 0..6 sum the 7 accumulators exactly; the
 // children's lobes are gathered into shared memory; if more than K remain, SGGX-H runs with
 // lane = slice for sigma (32 slices = 32 lanes) and lane = pair for distances and argmin.
-#include <cub/cub.cuh>
-
 #include <cmath>
 
 #include "vox_internal.cuh"
@@ -1053,62 +1051,6 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     return VOX_OK;
 }
 
-// Input iterator of the run-head flags of a sorted child key array (parent = key >> 3).
-struct HeadFlagIn {
-    const uint64_t* key;
-    int64_t base;
-    typedef std::random_access_iterator_tag iterator_category;
-    typedef uint32_t value_type;
-    typedef int64_t difference_type;
-    typedef const uint32_t* pointer;
-    typedef uint32_t reference;
-    __host__ __device__ uint32_t operator[](int64_t j) const {
-        const int64_t i = base + j;
-        return (i == 0 || (key[i] >> 3) != (key[i - 1] >> 3)) ? 1u : 0u;
-    }
-    __host__ __device__ uint32_t operator*() const { return (*this)[0]; }
-    __host__ __device__ HeadFlagIn operator+(int64_t d) const { return HeadFlagIn{key, base + d}; }
-};
-
-// Output "iterator" of that scan: position i receives the inclusive head count; a head writes
-// its parent's start (child index) and key; the last position closes start[] and the total.
-struct RunHeadOut {
-    const uint64_t* key;
-    uint32_t* start;
-    uint64_t* pkey;
-    uint64_t n;
-    uint32_t* total;
-    int64_t base;
-    struct Ref {
-        const uint64_t* key;
-        uint32_t* start;
-        uint64_t* pkey;
-        uint64_t n;
-        uint32_t* total;
-        int64_t i;
-        __device__ const Ref& operator=(uint32_t incl) const {
-            const uint64_t k = key[i];
-            if (i == 0 || (k >> 3) != (key[i - 1] >> 3)) {
-                start[incl - 1] = (uint32_t)i;
-                pkey[incl - 1] = k >> 3;
-            }
-            if ((uint64_t)i == n - 1) {
-                start[incl] = (uint32_t)n;
-                *total = incl;
-            }
-            return *this;
-        }
-    };
-    typedef std::random_access_iterator_tag iterator_category;
-    typedef uint32_t value_type;
-    typedef int64_t difference_type;
-    typedef void pointer;
-    typedef Ref reference;
-    __host__ __device__ Ref operator[](int64_t j) const { return Ref{key, start, pkey, n, total, base + j}; }
-    __host__ __device__ Ref operator*() const { return (*this)[0]; }
-    __host__ __device__ RunHeadOut operator+(int64_t d) const { return RunHeadOut{key, start, pkey, n, total, base + d}; }
-};
-
 vox_status build_level(vox_ctx* c, int l) {
     Level& C = c->lv[l - 1];
     Level& P = c->lv[l];
@@ -1118,25 +1060,17 @@ vox_status build_level(vox_ctx* c, int l) {
     const uint32_t K = c->K;
     if (n == 0) return VOX_OK;
     timer_begin(c, c->t_lodscan);
-    // one fused pass: run-head flags computed from the child keys on the fly (input iterator),
-    // their inclusive count scanned, and each head's parent start and key scattered by the
-    // output iterator -- no flag or count arrays. start / P.key are sized by n >= V.
+    // one single-pass scan (k_scan.cu): run-head flags computed from the child keys on the fly,
+    // each head's parent start and key scattered by the scan's output -- no flag or count
+    // arrays. start / P.key are sized by n >= V.
     uint32_t* start = nullptr;
     uint32_t* total = nullptr;
-    void* tmp = nullptr;
-    size_t tb = 0;
     CK(dalloc(c, (void**)&start, (n + 1) * 4));
     CK(dalloc(c, (void**)&P.key, n * 8));
     CK(dalloc(c, (void**)&total, 16));
-    HeadFlagIn in{C.key, 0};
-    RunHeadOut out{C.key, start, P.key, n, total, 0};
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int64_t)n, c->stream));
-    CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int64_t)n, c->stream));
-    c->st.launches += 2;
+    CK(scan_run_heads(c, C.key, n, start, P.key, total));
     uint32_t V = 0;
     CK(readback(c, {{&V, total, 4}}));
-    dfree(c, tmp);
     dfree(c, total);
     timer_end(c, c->t_lodscan);
     P.n = V;

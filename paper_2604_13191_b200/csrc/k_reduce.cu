@@ -1,54 +1,11 @@
 // k_reduce.cu -- gathering (§3.3 "ordered by second level block ID ... detect the
-// vector positions where the ID changes") as a device radix sort of (Morton key, payload)
-// pairs followed by a segmented reduction into exact fixed-point accumulators
-// (docs/PREDICATES.md §8). Also merges a new leaf set into an existing one (D19).
-//
-// The per-call path is the binned reduce below (no sort). CUB (header-only, CUDA 12.9) is
-// used for exclusive scans and, only when a second voxelize call is merged into an existing
-// leaf set, for the merge sort.
-#include <cub/cub.cuh>
-
+// vector positions where the ID changes"): the pairs of a call, appended per Morton bin by the
+// emit kernels, are ranked within their bin and reduced into exact fixed-point accumulators
+// (docs/PREDICATES.md §8) -- no global sort. Also merges a new leaf set into an existing one
+// (D19) by a merge of the two sorted key arrays.
 #include "vox_internal.cuh"
 
 namespace vox {
-
-__global__ void k_heads(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ flags) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
-}
-
-// heads -> start offsets of each run; start[V] = n.
-__global__ void k_starts(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ incl, uint64_t n,
-                         uint32_t* __restrict__ start) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (flags[i]) start[incl[i] - 1] = (uint32_t)i;
-        if (i == n - 1) start[incl[i]] = (uint32_t)n;
-    }
-}
-
-// One thread per voxel of a merge: sum the accumulator rows of its run (rows < n0 come from
-// the old leaf, the rest from the new one).
-__global__ void k_sum_rows(const uint32_t* __restrict__ start, uint64_t V, const uint64_t* __restrict__ keys,
-                           const uint32_t* __restrict__ idx, const long long* __restrict__ accA, uint64_t n0,
-                           const long long* __restrict__ accB, uint64_t* __restrict__ okey,
-                           long long* __restrict__ oacc) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = start[v], e = start[v + 1];
-        long long a[7] = {0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t i = s; i < e; i++) {
-            const uint64_t r = idx[i];
-            const long long* src = r < n0 ? accA + 7 * r : accB + 7 * (r - n0);
-            for (int q = 0; q < 7; q++) a[q] += src[q];
-        }
-        okey[v] = keys[s];
-        for (int q = 0; q < 7; q++) oacc[7 * v + q] = a[q];
-    }
-}
-
-__global__ void k_iota(uint32_t* __restrict__ p, uint64_t n) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        p[i] = (uint32_t)i;
-}
 
 static unsigned grid_for(uint64_t n, int threads = 256) {
     uint64_t b = (n + threads - 1) / threads;
@@ -66,30 +23,59 @@ static unsigned grid_for(uint64_t n, int threads = 256) {
         }                                                          \
     } while (0)
 
-// Runs of equal keys in sorted keys[0..n): returns V and start[V+1] (caller frees).
-static vox_status find_runs(vox_ctx* c, const uint64_t* keys, uint64_t n, uint32_t** start_out, uint64_t* V_out) {
-    uint32_t *flags = nullptr, *incl = nullptr, *start = nullptr;
-    void* tmp = nullptr;
-    size_t tb = 0;
-    CK(dalloc(c, (void**)&flags, n * 4));
-    CK(dalloc(c, (void**)&incl, n * 4));
-    k_heads<<<grid_for(n), 256, 0, c->stream>>>(keys, n, flags);
-    c->st.launches++;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flags, incl, (int64_t)n, c->stream));
-    CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceScan::InclusiveSum(tmp, tb, flags, incl, (int64_t)n, c->stream));
-    c->st.launches += 2;   // scan init + scan
-    uint32_t V32 = 0;
-    CK(readback(c, {{&V32, incl + n - 1, 4}}));
-    CK(dalloc(c, (void**)&start, ((uint64_t)V32 + 1) * 4));
-    k_starts<<<grid_for(n), 256, 0, c->stream>>>(flags, incl, n, start);
-    c->st.launches++;
-    dfree(c, tmp);
-    dfree(c, incl);
-    dfree(c, flags);
-    *start_out = start;
-    *V_out = V32;
-    return VOX_OK;
+// ---------------------------------------------------------------- merge of two leaf sets (D19)
+// A (the existing leaves, n0) and B (the new call's, V) are sorted with unique keys. In the
+// merged order (equal keys: A first), a_i sits at i + |{b < a_i}| and b_j at j + |{a < b_j}|;
+// a key present in both becomes one voxel, so every position is shifted down by the number of
+// such duplicate keys before it (an exclusive scan over A of dup_i). A duplicate b_j lands on
+// its a_i's slot and adds its accumulators (exact integer sums).
+
+// number of keys of k[0..n) below key (lower bound)
+__device__ __forceinline__ uint64_t lower_bound(const uint64_t* __restrict__ k, uint64_t n, uint64_t key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (k[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_merge_rank(const uint64_t* __restrict__ ka, uint64_t n0, const uint64_t* __restrict__ kb,
+                             uint64_t V, unsigned* __restrict__ dup, uint32_t* __restrict__ jb) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n0; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = lower_bound(kb, V, ka[i]);
+        jb[i] = (uint32_t)j;
+        dup[i] = (j < V && kb[j] == ka[i]) ? 1u : 0u;
+    }
+}
+
+__global__ void k_merge_write_a(const uint64_t* __restrict__ ka, const long long* __restrict__ aa, uint64_t n0,
+                                const uint32_t* __restrict__ jb, const unsigned* __restrict__ dscan,
+                                uint64_t* __restrict__ okey, long long* __restrict__ oacc) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n0; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = i + jb[i] - dscan[i];
+        okey[u] = ka[i];
+#pragma unroll
+        for (int e = 0; e < 7; e++) oacc[7 * u + e] = aa[7 * i + e];
+    }
+}
+
+__global__ void k_merge_write_b(const uint64_t* __restrict__ ka, uint64_t n0, const uint64_t* __restrict__ kb,
+                                const long long* __restrict__ ba, uint64_t V, const unsigned* __restrict__ dscan,
+                                uint64_t* __restrict__ okey, long long* __restrict__ oacc) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < V; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = lower_bound(ka, n0, kb[j]);
+        const uint64_t u = j + i - dscan[i];
+        if (i < n0 && ka[i] == kb[j]) {   // the key is in both sets: add into a_i's voxel
+#pragma unroll
+            for (int e = 0; e < 7; e++) oacc[7 * u + e] += ba[7 * j + e];
+        } else {
+            okey[u] = kb[j];
+#pragma unroll
+            for (int e = 0; e < 7; e++) oacc[7 * u + e] = ba[7 * j + e];
+        }
+    }
 }
 
 vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t V) {
@@ -130,39 +116,30 @@ vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t
         return VOX_OK;
     } else {
         timer_begin(c, c->t_merge);
-        const uint64_t n0 = L0.n, tot = n0 + V;
-        uint64_t *k0 = nullptr, *k1 = nullptr;
-        uint32_t *i0 = nullptr, *i1 = nullptr;
-        void* tmp = nullptr;
-        size_t tb = 0;
-        CK(dalloc(c, (void**)&k0, tot * 8));
-        CK(dalloc(c, (void**)&k1, tot * 8));
-        CK(dalloc(c, (void**)&i0, tot * 4));
-        CK(dalloc(c, (void**)&i1, tot * 4));
-        CK(cudaMemcpyAsync(k0, L0.key, n0 * 8, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(k0 + n0, nkey, V * 8, cudaMemcpyDeviceToDevice, c->stream));
-        k_iota<<<grid_for(tot), 256, 0, c->stream>>>(i0, tot);
-        c->st.launches++;
-        cub::DoubleBuffer<uint64_t> dk(k0, k1);
-        cub::DoubleBuffer<uint32_t> dv(i0, i1);
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int64_t)tot, 0, 3 * c->g.logN, c->stream));
-        CK(dalloc(c, &tmp, tb));
-        CK(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)tot, 0, 3 * c->g.logN, c->stream));
-        c->st.launches += 2 + (3 * c->g.logN + 7) / 8;
-        uint32_t* start = nullptr;
-        uint64_t VM = 0;
-        vox_status s = find_runs(c, dk.Current(), tot, &start, &VM);
-        if (s != VOX_OK) return s;
+        const uint64_t n0 = L0.n;
+        unsigned* dup = nullptr;
+        unsigned* dscan = nullptr;
+        uint32_t* jb = nullptr;
+        CK(dalloc(c, (void**)&dup, (n0 + 1) * 4));
+        CK(dalloc(c, (void**)&dscan, (n0 + 1) * 4));
+        CK(dalloc(c, (void**)&jb, n0 * 4));
+        CK(cudaMemsetAsync(dup + n0, 0, 4, c->stream));
+        k_merge_rank<<<grid_for(n0), 256, 0, c->stream>>>(L0.key, n0, nkey, V, dup, jb);
+        CK(scan_excl_u32(c, dup, dscan, n0 + 1));
+        unsigned D = 0;
+        CK(readback(c, {{&D, dscan + n0, 4}}));
+        const uint64_t VM = n0 + V - D;
         uint64_t* mkey = nullptr;
         long long* macc = nullptr;
         CK(dalloc(c, (void**)&mkey, VM * 8));
         CK(dalloc(c, (void**)&macc, VM * 56));
-        k_sum_rows<<<grid_for(VM), 256, 0, c->stream>>>(start, VM, dk.Current(), dv.Current(), L0.acc, n0, nacc,
-                                                         mkey, macc);
-        c->st.launches++;
-        dfree(c, start);
-        dfree(c, tmp);
-        dfree(c, k0); dfree(c, k1); dfree(c, i0); dfree(c, i1);
+        k_merge_write_a<<<grid_for(n0), 256, 0, c->stream>>>(L0.key, L0.acc, n0, jb, dscan, mkey, macc);
+        k_merge_write_b<<<grid_for(V), 256, 0, c->stream>>>(L0.key, n0, nkey, nacc, V, dscan, mkey, macc);
+        c->st.launches += 3;
+        CK(cudaGetLastError());
+        dfree(c, dup);
+        dfree(c, dscan);
+        dfree(c, jb);
         dfree(c, nkey);
         dfree(c, nacc);
         free_level(c, L0);
@@ -192,13 +169,6 @@ __global__ void k_group_sum(const unsigned long long* __restrict__ Wb, uint64_t 
     }
 }
 
-__global__ void k_bin_caps(const unsigned long long* __restrict__ Wb, uint64_t nb, int gshift, uint64_t lo,
-                           uint64_t hi, unsigned long long* __restrict__ caps) {
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= nb; b += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t top = b >> gshift;
-        caps[b] = (b < nb && top >= lo && top < hi) ? Wb[b] : 0ull;
-    }
-}
 
 constexpr int BIN_THREADS = 128;
 
@@ -544,20 +514,11 @@ vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigne
                        uint64_t* cap_out) {
     const uint64_t nb = 1ull << (3 * (c->g.logN - Lb));
     const int gshift = 3 * (c->g.logN - Lb - c->T);
-    unsigned long long *caps = nullptr, *off = nullptr;
-    void* tmp = nullptr;
-    size_t tb = 0;
-    CK(dalloc(c, (void**)&caps, (nb + 1) * 8));
+    unsigned long long* off = nullptr;
     CK(dalloc(c, (void**)&off, (nb + 1) * 8));
-    k_bin_caps<<<grid_for(nb + 1), 256, 0, c->stream>>>(Wb, nb, gshift, c->cell_lo, c->cell_hi, caps);
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, caps, off, (int64_t)(nb + 1), c->stream));
-    CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, caps, off, (int64_t)(nb + 1), c->stream));
-    c->st.launches += 3;
+    CK(scan_bin_caps(c, Wb, nb, gshift, c->cell_lo, c->cell_hi, off));   // caps of the rank's cells, scanned
     unsigned long long cap = 0;
     CK(readback(c, {{&cap, off + nb, 8}}));
-    dfree(c, tmp);
-    dfree(c, caps);
     *off_out = off;
     *cap_out = cap;
     return VOX_OK;
@@ -570,8 +531,6 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     unsigned* vcount = nullptr;
     unsigned* voff = nullptr;
     unsigned long long* npairs = nullptr;
-    void* tmp = nullptr;
-    size_t tb = 0;
     timer_begin(c, c->t_sort);
     CK(dalloc(c, (void**)&vcount, (nb + 1) * 4));
     CK(dalloc(c, (void**)&voff, (nb + 1) * 4));
@@ -585,10 +544,8 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     const unsigned grid = (unsigned)std::min<uint64_t>(nb, 148ull * 16);
     k_bin_count<<<grid, BIN_THREADS, words * 4, c->stream>>>(keys, bins.off, bins.cnt, alist, nact, lbits, vcount,
                                                              npairs);
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, vcount, voff, (int64_t)(nb + 1), c->stream));
-    CK(dalloc(c, &tmp, tb));
-    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, vcount, voff, (int64_t)(nb + 1), c->stream));
-    c->st.launches += 4;
+    CK(scan_excl_u32(c, vcount, voff, nb + 1));
+    c->st.launches += 2;
     unsigned V = 0;
     unsigned long long P = 0;
     CK(readback(c, {{&V, voff + nb, 4}, {&P, npairs, 8}}));
@@ -617,7 +574,6 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     c->st.launches += 2;
     CK(cudaGetLastError());
     timer_end(c, c->t_reduce);
-    dfree(c, tmp);
     dfree(c, vcount);
     dfree(c, voff);
     dfree(c, npairs);

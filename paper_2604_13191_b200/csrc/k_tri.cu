@@ -2,7 +2,6 @@
 // half-open clipped area emit (k_tri_emit). docs/PREDICATES.md §1, §3, §6, §7 (north star:
 // triangle-box SAT; P:225-228 area-weighted triangle sampling whose continuous limit is the
 // clipped area; P:179 face normals, P:183/P:549 tangent mode).
-#include <cub/cub.cuh>
 
 #include "vox_internal.cuh"
 
@@ -314,8 +313,6 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
                             uint64_t* keys, uint64_t* vals, float4* ptab) {
     TriSetup* ts = nullptr;
     unsigned long long *tcnt = nullptr, *toff = nullptr;
-    void* tmp = nullptr;
-    size_t tb = 0;
     cudaError_t e;
     if ((e = dalloc(c, (void**)&ts, T * sizeof(TriSetup))) != cudaSuccess) return e;
     if ((e = dalloc(c, (void**)&tcnt, (T + 1) * 8)) != cudaSuccess) return e;
@@ -324,14 +321,10 @@ cudaError_t launch_tri_emit(vox_ctx* c, const float* tri, const float* dirs, uin
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     k_tri_setup<<<(unsigned)blocks, 256, 0, c->stream>>>(tri, dirs, T, c->g, sh, ts, tcnt, ptab);
     if ((e = cudaMemsetAsync(tcnt + T, 0, 8, c->stream)) != cudaSuccess) return e;
-    if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, tcnt, toff, (int64_t)(T + 1), c->stream)) != cudaSuccess)
-        return e;
-    if ((e = dalloc(c, &tmp, tb)) != cudaSuccess) return e;
-    if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, tcnt, toff, (int64_t)(T + 1), c->stream)) != cudaSuccess) return e;
+    if ((e = scan_excl_u64(c, tcnt, toff, T + 1)) != cudaSuccess) return e;
     k_tri_emit<<<148u * 16, TRI_WARPS * 32, 0, c->stream>>>(ts, toff, T, c->g, sh, bins, keys, vals, c->d_flags);
-    c->st.launches += 4;
+    c->st.launches += 2;   // + the scan's own
     e = cudaGetLastError();
-    dfree(c, tmp);
     dfree(c, toff);
     dfree(c, tcnt);
     dfree(c, ts);

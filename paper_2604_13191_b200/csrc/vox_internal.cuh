@@ -262,6 +262,13 @@ vox_status merge_into_leaf(vox_ctx* c, uint64_t* nkey, long long* nacc, uint64_t
 vox_status bin_topcells(vox_ctx* c, const unsigned long long* Wb, int Lb, std::vector<uint64_t>& WT);
 vox_status bin_offsets(vox_ctx* c, const unsigned long long* Wb, int Lb, unsigned long long** off_out,
                        uint64_t* cap_out);
+// single-pass exclusive scans, decoupled look-back (k_scan.cu)
+cudaError_t scan_excl_u64(vox_ctx* c, const unsigned long long* in, unsigned long long* out, uint64_t n);
+cudaError_t scan_excl_u32(vox_ctx* c, const unsigned* in, unsigned* out, uint64_t n);
+cudaError_t scan_bin_caps(vox_ctx* c, const unsigned long long* Wb, uint64_t nb, int gshift, uint64_t lo, uint64_t hi,
+                          unsigned long long* off);
+cudaError_t scan_run_heads(vox_ctx* c, const uint64_t* key, uint64_t n, uint32_t* start, uint64_t* pkey,
+                           uint32_t* total);
 // LoD (k_lod.cu)
 vox_status build_level(vox_ctx* c, int l);
 void upload_theta(vox_ctx* c);
