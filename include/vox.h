@@ -205,6 +205,12 @@ vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_
 vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                                 uint8_t* ncl, float* cl, void* stream);
 
+/* Debug builds (-DVOX_DEBUG): OR of the bounds-check bits that fired since the last call
+ * (bit 0 emit survivor FIFO, 1 bin rank, 2 bin slot, 3 warp-kernel lobe count, 4 quad lobe
+ * count, 5 half lobe count, 7 level-1 staged rows), cleared by the read; release builds
+ * always return 0. Synchronous (reads device memory). */
+vox_status vox_debug_flags(uint32_t* out);
+
 /* Copy a level's exact accumulators acc [n][7] (int64, quantum 2^-32; device or host). */
 vox_status vox_copy_level_acc(vox_ctx* ctx, uint32_t level, int64_t* acc);
 

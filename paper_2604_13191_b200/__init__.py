@@ -20,6 +20,9 @@ __all__ = ["Vox", "VoxError", "lib", "plan_shards", "theta_table", "record_bytes
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvox.so")
+# VOX_DEBUG_LIB=1 loads the bounds-checked build libvox_dbg.so (tools/debug_checks.sh builds it)
+if os.environ.get("VOX_DEBUG_LIB") == "1":
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libvox_dbg.so")
 
 STATUS = {0: "VOX_OK", 1: "VOX_ERR_INVALID_ARG", 2: "VOX_ERR_DEGENERATE_BBOX", 3: "VOX_ERR_STATE",
           4: "VOX_ERR_OOM", 5: "VOX_ERR_CAPACITY", 6: "VOX_ERR_CUDA", 7: "VOX_ERR_LEVEL", 8: "VOX_ERR_COMM"}
@@ -77,6 +80,7 @@ def lib():
     L.vox_build_lod.argtypes = [vp, u32]
     L.vox_built_levels.argtypes = [vp, C.POINTER(u32)]
     L.vox_level_size.argtypes = [vp, u32, C.POINTER(u64)]
+    L.vox_debug_flags.argtypes = [C.POINTER(u32)]
     L.vox_read_level.argtypes = [vp, u32, C.POINTER(_View)]
     L.vox_copy_level.argtypes = [vp, u32, vp, vp, vp, vp, vp]
     L.vox_copy_level_acc.argtypes = [vp, u32, vp]
@@ -102,7 +106,7 @@ def lib():
     L.vox_last_error.argtypes = [vp]
     L.vox_destroy.argtypes = [vp]
     for name in ("vox_create", "vox_voxelize_fibers", "vox_voxelize_triangles", "vox_voxelize_fibers_host",
-                 "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_level_size", "vox_read_level",
+                 "vox_voxelize_triangles_host", "vox_build_lod", "vox_built_levels", "vox_level_size", "vox_debug_flags", "vox_read_level",
                  "vox_copy_level", "vox_copy_level_acc", "vox_copy_level_async", "vox_encode_level", "vox_sample_splines",
                  "vox_sample_triangles", "vox_density_fibers", "vox_density_triangles", "vox_density_level", "vox_export_level", "vox_import_level", "vox_plan_shards", "vox_theta_table",
                  "vox_hist_tables", "vox_stats_get", "vox_stats_reset", "vox_sync", "vox_trim"):

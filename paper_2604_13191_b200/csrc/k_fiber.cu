@@ -6,6 +6,8 @@
 
 namespace vox {
 
+VOX_DEBUG_TU(fiber)
+
 struct SegGeom {
     float a[3], b[3], rg;
     bool culled;
@@ -346,7 +348,10 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                 ent = make_int4(o, (int)i, (int)j, (int)k);
             }
             const unsigned bal = __ballot_sync(0xffffffffu, surv);
-            if (surv) s_q[wib][qn + __popc(bal & ((1u << lane) - 1u))] = ent;
+            if (surv) {
+                VOX_DCHECK(qn + __popc(bal & ((1u << lane) - 1u)) < 64, 0);   // survivor FIFO
+                s_q[wib][qn + __popc(bal & ((1u << lane) - 1u))] = ent;
+            }
             qn += __popc(bal);
             __syncwarp();
             if (qn >= 32) {

@@ -12,6 +12,8 @@
 
 namespace vox {
 
+VOX_DEBUG_TU(lod)
+
 __constant__ float c_coef[VOX_SLICES][6];
 
 // PREDICATES §9 slice table: spherical Fibonacci on the upper hemisphere, evaluated in fp64,
@@ -217,6 +219,7 @@ k_lod_prep_leaf(const long long* __restrict__ cacc,
         mbar_wait(&s_bar[wib][b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const long long* rows = wbase + (size_t)b * PREP_ROWW + ((7 * (uint64_t)cs) & 1);
+        VOX_DCHECK(lane >= np || 7 * c1 + (int)((7 * (uint64_t)cs) & 1) <= PREP_ROWW, 7);   // staged child rows
         bool hard = false;
         if (lane < np) {
             const uint64_t p = p0 + lane;
@@ -346,6 +349,7 @@ __device__ __forceinline__ int gather_lobes(const uint32_t* __restrict__ start, 
         const unsigned bal = __ballot_sync(mask, has);
         if (has) {
             const int c = n + __popc(bal & ((1u << lane) - 1u));
+            VOX_DCHECK(c < 8 * K, 3);
 #pragma unroll
             for (int e = 0; e < 7; e++) out[7 * c + e] = src[e];
         }
@@ -458,6 +462,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 const unsigned gm = (__ballot_sync(0xffffffffu, has) >> (8 * g)) & 0xffu;
                 if (has) {
                     const int c = n + __popc(gm & ((1u << l) - 1u));
+                    VOX_DCHECK(c < 8, 4);
 #pragma unroll
                     for (int e = 0; e < 7; e++) lobe[c][e] = src[e];
                 }
@@ -811,6 +816,7 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             const unsigned bal = (__ballot_sync(0xffffffffu, has) >> (16 * g)) & 0xffffu;
             if (has) {
                 const int c = n + __popc(bal & ((1u << l) - 1u));
+                VOX_DCHECK(c < 16, 5);
 #pragma unroll
                 for (int e = 0; e < 7; e++) H.lobe[c][e] = src[e];
             }
@@ -1052,6 +1058,10 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
 }
 
 vox_status build_level(vox_ctx* c, int l) {
+    static const char* names[VOX_MAX_LEVELS] = {"level 0", "level 1", "level 2", "level 3", "level 4", "level 5", "level 6",
+                                                "level 7", "level 8", "level 9", "level 10", "level 11", "level 12",
+                                                "level 13"};
+    VOX_RANGE(names[l < VOX_MAX_LEVELS ? l : 0]);
     Level& C = c->lv[l - 1];
     Level& P = c->lv[l];
     free_level(c, P);

@@ -7,6 +7,8 @@
 
 namespace vox {
 
+VOX_DEBUG_TU(reduce)
+
 static unsigned grid_for(uint64_t n, int threads = 256) {
     uint64_t b = (n + threads - 1) / threads;
     if (b > 148ull * 32) b = 148ull * 32;
@@ -350,7 +352,10 @@ k_bin_reduce(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ val
             // scatter pair indices by rank; afterwards cur[r] = end of rank r's run
             for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
                 const unsigned r = key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask));
-                sidx[atomicAdd(&cur[r], 1u)] = (unsigned short)i;
+                VOX_DCHECK(r < V, 1);
+                const unsigned slot = atomicAdd(&cur[r], 1u);
+                VOX_DCHECK(slot < n && slot < BIN_NMAX, 2);
+                sidx[slot] = (unsigned short)i;
             }
             __syncthreads();
             for (unsigned r = threadIdx.x; r < V; r += blockDim.x) {
@@ -481,7 +486,10 @@ k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
         __syncwarp();
         for (unsigned i = lane; i < n; i += 32) {
             const unsigned r = key_rank(bm, wpre, (unsigned)(keys[o + i] & lmask));
-            sidx[atomicAdd(&cur[r], 1u)] = (unsigned short)i;
+            VOX_DCHECK(r < V, 1);
+            const unsigned slot = atomicAdd(&cur[r], 1u);
+            VOX_DCHECK(slot < n && slot < WB_NMAX, 2);
+            sidx[slot] = (unsigned short)i;
         }
         __syncwarp();
         for (unsigned r = lane; r < V; r += 32) {

@@ -302,6 +302,7 @@ const char* vox_status_str(vox_status s) {
 const char* vox_last_error(vox_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
 
 vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], const vox_options* opt) {
+    VOX_RANGE("vox_create");
     if (!out || !bbox) return VOX_ERR_INVALID_ARG;
     *out = nullptr;
     if (grid_res < 2 || grid_res > 8192 || (grid_res & (grid_res - 1))) return VOX_ERR_INVALID_ARG;
@@ -556,6 +557,7 @@ static cudaError_t emit_tris(vox_ctx* c, const float* tri, const float* dirs, ui
 }
 
 vox_status vox_voxelize_fibers(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    VOX_RANGE("vox_voxelize_fibers");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (S == 0) return VOX_OK;
@@ -577,6 +579,7 @@ vox_status vox_voxelize_fibers(vox_ctx* c, const float* segments, const float* r
 }
 
 vox_status vox_voxelize_triangles(vox_ctx* c, const float* tris, const float* dirs, uint64_t T) {
+    VOX_RANGE("vox_voxelize_triangles");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (T == 0) return VOX_OK;
@@ -609,6 +612,7 @@ static cudaError_t emit_sampled_tris(vox_ctx* c, const float* tri, const float* 
 }
 
 vox_status vox_sample_splines(vox_ctx* c, const float* ctrl, const float* radii, uint64_t S, uint32_t n) {
+    VOX_RANGE("vox_sample_splines");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (S == 0) return VOX_OK;
@@ -631,6 +635,7 @@ vox_status vox_sample_splines(vox_ctx* c, const float* ctrl, const float* radii,
 }
 
 vox_status vox_sample_triangles(vox_ctx* c, const float* tris, const float* dirs, uint64_t T, uint32_t budget) {
+    VOX_RANGE("vox_sample_triangles");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (T == 0) return VOX_OK;
@@ -658,6 +663,7 @@ vox_status vox_sample_triangles(vox_ctx* c, const float* tris, const float* dirs
 }
 
 vox_status vox_voxelize_fibers_host(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    VOX_RANGE("vox_voxelize_fibers_host");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (S == 0) return VOX_OK;
@@ -674,6 +680,7 @@ vox_status vox_voxelize_fibers_host(vox_ctx* c, const float* segments, const flo
 }
 
 vox_status vox_voxelize_triangles_host(vox_ctx* c, const float* tris, const float* dirs, uint64_t T) {
+    VOX_RANGE("vox_voxelize_triangles_host");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->state == ST_LOD) return VOX_ERR_STATE;
     if (T == 0) return VOX_OK;
@@ -692,6 +699,7 @@ vox_status vox_voxelize_triangles_host(vox_ctx* c, const float* tris, const floa
 }
 
 vox_status vox_build_lod(vox_ctx* c, uint32_t levels) {
+    VOX_RANGE("vox_build_lod");
     if (!c) return VOX_ERR_INVALID_ARG;
     if ((int)levels > c->g.logN) return VOX_ERR_LEVEL;
     vox_status s = ensure_dev(c);
@@ -724,6 +732,7 @@ vox_status vox_level_size(vox_ctx* c, uint32_t level, uint64_t* out) {
 }
 
 vox_status vox_read_level(vox_ctx* c, uint32_t level, vox_level_view* out) {
+    VOX_RANGE("vox_read_level");
     if (!c || !out) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     vox_status s = ensure_f32(c, (int)level);   // the build keeps only the exact accumulators
@@ -779,6 +788,7 @@ static vox_status density_prepare(vox_ctx* c) {
 }
 
 vox_status vox_density_fibers(vox_ctx* c, const float* segments, const float* radii, uint64_t S) {
+    VOX_RANGE("vox_density_fibers");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (S && (!segments || !radii)) return VOX_ERR_INVALID_ARG;
     vox_status s = ensure_dev(c);
@@ -793,6 +803,7 @@ vox_status vox_density_fibers(vox_ctx* c, const float* segments, const float* ra
 }
 
 vox_status vox_density_triangles(vox_ctx* c, const float* tris, uint64_t T) {
+    VOX_RANGE("vox_density_triangles");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (T && !tris) return VOX_ERR_INVALID_ARG;
     vox_status s = ensure_dev(c);
@@ -807,6 +818,7 @@ vox_status vox_density_triangles(vox_ctx* c, const float* tris, uint64_t T) {
 }
 
 vox_status vox_density_level(vox_ctx* c, uint32_t level, float* occ, float* axis, uint64_t* masks) {
+    VOX_RANGE("vox_density_level");
     if (!c) return VOX_ERR_INVALID_ARG;
     if (c->dmask_levels < 0) return VOX_ERR_STATE;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
@@ -829,6 +841,7 @@ vox_status vox_density_level(vox_ctx* c, uint32_t level, float* occ, float* axis
 }
 
 vox_status vox_encode_level(vox_ctx* c, uint32_t level, uint8_t* sggx6, uint8_t* cl6, uint8_t* flags) {
+    VOX_RANGE("vox_encode_level");
     if (!c || !sggx6) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     timer_begin(c, c->t_encode);
@@ -839,6 +852,7 @@ vox_status vox_encode_level(vox_ctx* c, uint32_t level, uint8_t* sggx6, uint8_t*
 }
 
 vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass, float* m6, uint8_t* ncl, float* cl) {
+    VOX_RANGE("vox_copy_level");
     if (!c) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     const Level& L = c->lv[level];
@@ -874,6 +888,7 @@ vox_status vox_copy_level(vox_ctx* c, uint32_t level, uint64_t* key, float* mass
 
 vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float* mass, float* m6, uint8_t* ncl,
                                 float* cl, void* stream) {
+    VOX_RANGE("vox_copy_level_async");
     if (!c) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     if (level == 0 && (ncl || cl)) return VOX_ERR_INVALID_ARG;
@@ -933,6 +948,7 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
 }
 
 vox_status vox_copy_level_acc(vox_ctx* c, uint32_t level, int64_t* acc) {
+    VOX_RANGE("vox_copy_level_acc");
     if (!c || !acc) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     const Level& L = c->lv[level];
@@ -943,6 +959,7 @@ vox_status vox_copy_level_acc(vox_ctx* c, uint32_t level, int64_t* acc) {
 }
 
 vox_status vox_export_level(vox_ctx* c, uint32_t level, void* buf, uint64_t* bytes) {
+    VOX_RANGE("vox_export_level");
     if (!c || !bytes) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->built) return VOX_ERR_LEVEL;
     const uint64_t need = c->lv[level].n * record_bytes(c->K);
@@ -957,6 +974,7 @@ vox_status vox_export_level(vox_ctx* c, uint32_t level, void* buf, uint64_t* byt
 }
 
 vox_status vox_import_level(vox_ctx* c, uint32_t level, const void* buf, uint64_t bytes) {
+    VOX_RANGE("vox_import_level");
     if (!c) return VOX_ERR_INVALID_ARG;
     if ((int)level > c->g.logN) return VOX_ERR_LEVEL;
     const uint64_t rb = record_bytes(c->K);
@@ -999,6 +1017,12 @@ vox_status vox_hist_tables(uint32_t N, float* u, uint8_t* perm, uint32_t* gap) {
     if (u) std::memcpy(u, hu.data(), hu.size() * sizeof(float));
     if (perm) std::memcpy(perm, hp.data(), hp.size());
     if (gap) std::memcpy(gap, hg.data(), hg.size() * sizeof(uint32_t));
+    return VOX_OK;
+}
+
+vox_status vox_debug_flags(uint32_t* out) {
+    if (!out) return VOX_ERR_INVALID_ARG;
+    *out = debug_read_fiber() | debug_read_reduce() | debug_read_lod();
     return VOX_OK;
 }
 
@@ -1046,6 +1070,7 @@ vox_status vox_stats_reset(vox_ctx* c) {
 }
 
 vox_status vox_trim(vox_ctx* c) {
+    VOX_RANGE("vox_trim");
     if (!c) return VOX_ERR_INVALID_ARG;
     CKS(ssync(c));
     vox_trim_stream(c->stream);
@@ -1059,12 +1084,14 @@ vox_status vox_trim(vox_ctx* c) {
 }
 
 vox_status vox_sync(vox_ctx* c) {
+    VOX_RANGE("vox_sync");
     if (!c) return VOX_ERR_INVALID_ARG;
     CKS(ssync(c));
     return VOX_OK;
 }
 
 void vox_destroy(vox_ctx* c) {
+    VOX_RANGE("vox_destroy");
     if (!c) return;
     ssync(c);
     release_mapped(c);

@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/vox.h"
 
 #define VOX_MAX_LEVELS 14
@@ -27,6 +29,43 @@
 #define VOX_EFLAG_OVERFLOW 16u
 
 namespace vox {
+
+// NVTX range for the lifetime of a scope (one per C-ABI call and per pyramid level), so an
+// nsys / ncu timeline shows the library's calls; a no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define VOX_RANGE(name) ::vox::NvtxRange vox_nvtx_range_(name)
+
+// Bounds checks of a debug build (-DVOX_DEBUG, e.g. VOX_NVCC_EXTRA=-DVOX_DEBUG): a failed check
+// sets bit `bit` of a per-translation-unit device word; vox_debug_flags ORs them (compute-
+// sanitizer is closed on the GPU pool, so the library checks its own shared-memory and slot
+// indices). Release builds compile the checks out.
+#ifdef VOX_DEBUG
+#define VOX_DEBUG_TU(name)                                                          \
+    static __device__ unsigned g_vox_dbg;                                           \
+    unsigned debug_read_##name() {                                                  \
+        unsigned v = 0;                                                             \
+        cudaMemcpyFromSymbol(&v, g_vox_dbg, 4);                                     \
+        const unsigned z = 0;                                                       \
+        cudaMemcpyToSymbol(g_vox_dbg, &z, 4);                                       \
+        return v;                                                                   \
+    }
+#define VOX_DCHECK(cond, bit)                                      \
+    do {                                                           \
+        if (!(cond)) atomicOr(&g_vox_dbg, 1u << (bit));            \
+    } while (0)
+#else
+#define VOX_DEBUG_TU(name) \
+    unsigned debug_read_##name() { return 0; }
+#define VOX_DCHECK(cond, bit) \
+    do {                      \
+    } while (0)
+#endif
+unsigned debug_read_fiber();
+unsigned debug_read_reduce();
+unsigned debug_read_lod();
 
 // ---------------------------------------------------------------- pinned helpers (PREDICATES)
 
