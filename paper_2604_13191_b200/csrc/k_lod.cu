@@ -365,6 +365,9 @@ __device__ __forceinline__ int gather_lobes(const uint32_t* __restrict__ start, 
 // registers, then the last three tree levels by xor-shuffles inside the group -- and kept in
 // a shared 28-entry table per parent; the lexicographic argmin (d, i, j) is a group reduce.
 constexpr int QUAD_WARPS = 4;
+#ifndef QUAD_MINB
+#define QUAD_MINB 6
+#endif
 
 __device__ __forceinline__ float part4(const float* a, const float* b) {
     return (fabsf(a[0] - b[0]) + fabsf(a[2] - b[2])) + (fabsf(a[1] - b[1]) + fabsf(a[3] - b[3]));
@@ -385,7 +388,7 @@ __device__ __forceinline__ unsigned long long group_min8(unsigned long long v) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(QUAD_WARPS * 32)
+__global__ void __launch_bounds__(QUAD_WARPS * 32, QUAD_MINB)
 k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ counts,
              const long long* __restrict__ cacc, const uint8_t* __restrict__ cncl,
              const long long* __restrict__ cclacc, int leaf, const uint32_t* __restrict__ start,
@@ -405,14 +408,15 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     long long(*lobe)[7] = s_lobe[wib][g];
     float(*Sg)[6] = s_S[wib][g];
     float* D = s_D[wib][g];
-    __shared__ __align__(16) float s_cf[32][6];
-    for (int x = threadIdx.x; x < 32 * 6; x += blockDim.x) s_cf[x / 6][x % 6] = c_coef[x / 6][x % 6];
+    __shared__ __align__(16) float s_cfl[8][4][6];   // [l][q][e] = coefficient e of slice l + 8 q
+    for (int x = threadIdx.x; x < 8 * 4 * 6; x += blockDim.x) {
+        const int ll = x / 24, q = (x / 6) % 4, e = x % 6;
+        s_cfl[ll][q][e] = c_coef[ll + 8 * q][e];
+    }
     __syncthreads();
-    float2 cf[4][3];   // coefficients of this lane's slices l, l+8, l+16, l+24
-#pragma unroll
-    for (int q = 0; q < 4; q++)
-#pragma unroll
-        for (int e = 0; e < 3; e++) cf[q][e] = reinterpret_cast<const float2*>(s_cf[l + 8 * q])[e];
+    // coefficients of this lane's slices l, l+8, l+16, l+24, read from shared memory at each use
+    // (keeps 24 registers free: occupancy is what the serial merge chains need)
+    const float2(*cf)[3] = reinterpret_cast<const float2(*)[3]>(s_cfl[l]);
     const unsigned small = counts[0];
     const unsigned nquad = (small + 3) / 4;
     for (unsigned qd = blockIdx.x * QUAD_WARPS + wib; qd < nquad; qd += gridDim.x * QUAD_WARPS) {

@@ -5,6 +5,7 @@
     python tools/diag.py shard   [world ...]       per-rank device time of config-4 Morton shards, one GPU
     python tools/diag.py maxsize [segments] [N]    config 5 point: device time, counts, memory
     python tools/diag.py density [segments]        device time of the sub-voxel density pass (NEXT-2)
+    python tools/diag.py overlap [parts]           config 4 as Morton parts on concurrent streams (host threads)
 """
 import os
 import sys
@@ -111,6 +112,42 @@ def density(n=10_000_000):
         st = v.stats()
         print("density ms", round(st["ms_density"], 2), "alloc ms", round(st["host_ms_alloc"], 2), flush=True)
         v.close()
+
+
+def overlap(parts=2):
+    """Wall time of config 4 (voxelize + local levels) as `parts` Morton shards of one GPU, run
+    one after the other on one stream vs concurrently (one host thread + stream per shard)."""
+    import threading
+    parts = int(parts)
+    c = gen.config(4)
+    S, R = _dev(c)
+    Lt = c["levels"] - 4
+
+    def one(rank, world, stream):
+        with torch.cuda.stream(stream):
+            v = Vox(c["grid_res"], c["bbox"], rank=rank, world=world, stream=stream)
+            v.voxelize_fibers(S, R)
+            v.build_lod(Lt if world > 1 else c["levels"])
+            stream.synchronize()
+            v.close()
+
+    streams = [torch.cuda.Stream() for _ in range(parts)]
+    for it in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        one(0, 1, streams[0])
+        t1 = time.perf_counter()
+        for r in range(parts):
+            one(r, parts, streams[0])
+        t2 = time.perf_counter()
+        th = [threading.Thread(target=one, args=(r, parts, streams[r])) for r in range(parts)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        t3 = time.perf_counter()
+        print(f"whole {1e3 * (t1 - t0):.1f} ms | {parts} shards sequential {1e3 * (t2 - t1):.1f} ms | "
+              f"concurrent {1e3 * (t3 - t2):.1f} ms", flush=True)
 
 
 if __name__ == "__main__":
