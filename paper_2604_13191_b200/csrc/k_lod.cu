@@ -99,6 +99,8 @@ __global__ void k_lod_prep(const long long* __restrict__ cacc,
                     }
                 }
             }
+            // unused slots are written as zeros: they are never read, but skipping them leaves
+            // partial sectors that cost more than the bytes (measured)
             for (int q = slot; q < K; q++)
                 for (int e = 0; e < 7; e++) pclacc[(p * K + q) * 7 + e] = 0;
             pncl[p] = (uint8_t)slot;
@@ -250,7 +252,8 @@ k_lod_prep_leaf(const long long* __restrict__ cacc,
         }
         const unsigned hmask = __ballot_sync(0xffffffffu, hard);
         __syncwarp();
-        // coalesced write-back: accumulators, lobes of the final (n <= K) parents
+        // coalesced write-back: accumulators, lobes of the final (n <= K) parents (zero slots
+        // included: whole sectors)
         for (int w = lane; w < np * 7; w += 32) pacc[7 * p0 + w] = sacc[w];
         for (int w = lane; w < np * K * 7; w += 32) {
             if ((hmask >> (w / (K * 7))) & 1u) continue;
@@ -1123,9 +1126,9 @@ __global__ void k_pack(uint64_t n, const uint64_t* __restrict__ key, const long 
         for (int e = 0; e < 7; e++) r[1 + e] = acc[7 * v + e];
         const int m = leaf ? (acc[7 * v] > 0) : ncl[v];
         r[8] = m;
-        for (int q = 0; q < K; q++)
+        for (int q = 0; q < K; q++)   // lobe slots >= ncl hold no data in the level: exported as 0
             for (int e = 0; e < 7; e++)
-                r[9 + 7 * q + e] = leaf ? (q == 0 && m ? acc[7 * v + e] : 0) : clacc[(v * K + q) * 7 + e];
+                r[9 + 7 * q + e] = q < m ? (leaf ? acc[7 * v + e] : clacc[(v * K + q) * 7 + e]) : 0;
     }
 }
 

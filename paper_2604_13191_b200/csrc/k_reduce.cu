@@ -256,7 +256,8 @@ __device__ __forceinline__ void bitmap_prefix(const unsigned* bm, unsigned* wpre
     __syncthreads();
 }
 
-__device__ __forceinline__ unsigned key_rank(const unsigned* bm, const unsigned* wpre, unsigned lk) {
+template <class W>
+__device__ __forceinline__ unsigned key_rank(const unsigned* bm, const W* wpre, unsigned lk) {
     const unsigned w = lk >> 5, bit = lk & 31;
     return wpre[w] + __popc(bm[w] & ((1u << bit) - 1u));
 }
@@ -419,11 +420,12 @@ k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
     extern __shared__ __align__(16) unsigned char s_raw[];
     const int words = lbits >= 5 ? (1 << (lbits - 5)) : 1;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const size_t per_warp = (size_t)2 * words * 4 + (WB_VMAX + 1) * 4 + WB_NMAX * 2;
+    // word prefixes as u16 (a warp bin has <= WB_VMAX keys): 2 B per bitmap word
+    const size_t per_warp = ((size_t)words * 6 + (WB_VMAX + 1) * 4 + WB_NMAX * 2 + 15) & ~(size_t)15;
     unsigned* bm = reinterpret_cast<unsigned*>(s_raw + wib * per_warp);
-    unsigned* wpre = bm + words;
-    unsigned* cur = wpre + words;
-    unsigned short* sidx = reinterpret_cast<unsigned short*>(cur + WB_VMAX + 1);
+    unsigned* cur = bm + words;
+    uint16_t* wpre = reinterpret_cast<uint16_t*>(cur + WB_VMAX + 1);
+    unsigned short* sidx = reinterpret_cast<unsigned short*>(wpre + words);
     const uint64_t lmask = (1ull << lbits) - 1ull;
     const unsigned na = *nact;
     for (unsigned ai = blockIdx.x * WB_WARPS + wib; ai < na; ai += gridDim.x * WB_WARPS) {
@@ -457,7 +459,7 @@ k_bin_reduce_warp(const uint64_t* __restrict__ keys, const uint64_t* __restrict_
             unsigned run = inc - loc;
             for (int q = 0; q < per; q++)
                 if (w0 + q < words) {
-                    wpre[w0 + q] = run;
+                    wpre[w0 + q] = (uint16_t)run;
                     run += __popc(bm[w0 + q]);
                 }
         }
@@ -569,7 +571,7 @@ vox_status reduce_bins(vox_ctx* c, const uint64_t* keys, const uint64_t* vals, B
     CK(dalloc(c, (void**)&big, nb * 4 + 4));
     unsigned* nbig = big + nb;
     CK(cudaMemsetAsync(nbig, 0, 4, c->stream));
-    const size_t wsm = (size_t)WB_WARPS * ((size_t)2 * words * 4 + (WB_VMAX + 1) * 4 + WB_NMAX * 2);
+    const size_t wsm = (size_t)WB_WARPS * (((size_t)words * 6 + (WB_VMAX + 1) * 4 + WB_NMAX * 2 + 15) & ~(size_t)15);
     CK(cudaFuncSetAttribute(k_bin_reduce_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
     const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + WB_WARPS - 1) / WB_WARPS, 148ull * 32);
     k_bin_reduce_warp<<<wgrid, WB_WARPS * 32, wsm, c->stream>>>(keys, vals, ptab, bins.off, bins.cnt, alist, nact,

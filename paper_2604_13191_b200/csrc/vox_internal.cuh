@@ -194,7 +194,7 @@ struct Level {
     uint64_t* key = nullptr;
     long long* acc = nullptr;   // [n][7]
     uint8_t* ncl = nullptr;     // [n]       (levels >= 1)
-    long long* clacc = nullptr; // [n][K][7] (levels >= 1)
+    long long* clacc = nullptr; // [n][K][7] (levels >= 1); slots q >= ncl are undefined (never read)
     float* mass = nullptr;      // [n]        fp32 view, valid iff f32
     float* m6 = nullptr;        // [n][6]     fp32 view, valid iff f32
     float* cl = nullptr;        // [n][K][7]  fp32 view (levels >= 1), valid iff f32
