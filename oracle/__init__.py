@@ -51,6 +51,7 @@ def lib():
         L.orc_add_fibers.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64]
         L.orc_add_triangles.argtypes = [C.c_void_p, f32p, f32p, C.c_uint64]
         L.orc_build.argtypes = [C.c_void_p, C.c_int]
+        L.orc_build_from.argtypes = [C.c_void_p, C.c_int, C.c_uint64, u64p, i64p, u8p, i64p, C.c_int]
         L.orc_level_size.restype = C.c_uint64
         L.orc_level_size.argtypes = [C.c_void_p, C.c_int]
         L.orc_level_copy.argtypes = [C.c_void_p, C.c_int, u64p, i64p, f32p, f32p, u8p, i64p, f32p]
@@ -186,6 +187,20 @@ class Oracle:
 
     def build(self, levels: int = 0):
         _check(lib().orc_build(self._h, int(levels)), "build")
+
+    def build_from(self, l0: int, key, acc, ncl, cl_acc, levels: int):
+        """Start the pyramid from given level-l0 records (sorted keys [n], exact acc [n,7],
+        ncl [n], lobe accumulators [n,k,7]; ignored for l0 = 0) and build levels l0+1..levels
+        with the same code as build() (test infrastructure: upper levels of workloads too large
+        for the oracle's voxelization)."""
+        key = np.ascontiguousarray(key, np.uint64)
+        n = len(key)
+        acc = np.ascontiguousarray(acc, np.int64).reshape(n, 7)
+        ncl = np.ascontiguousarray(ncl if ncl is not None else np.zeros(n), np.uint8)
+        cla = np.ascontiguousarray(cl_acc if cl_acc is not None else np.zeros((n, self.k, 7)), np.int64)
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        _check(lib().orc_build_from(self._h, int(l0), n, P(key, C.c_uint64), P(acc, C.c_int64), P(ncl, C.c_uint8),
+                                    P(cla, C.c_int64), int(levels)), "build_from")
 
     def level(self, l: int) -> dict:
         n = int(lib().orc_level_size(self._h, int(l)))

@@ -1344,12 +1344,12 @@ static int cmp_rec(const void* x, const void* y) {
 }
 
 /* Leaf (§8, §9 level 0) then levels 1..levels (§9). */
+static int build_up(orc_ctx* c, int levels);
+
 int orc_build(orc_ctx* c, int levels) {
     if (levels < 0 || levels > c->logN) return ORC_ERR_LEVEL;
     free_levels(c);
     const int K = c->K;
-    float theta[32][3], coef[32][6];
-    theta_table(theta, coef);
     /* level 0: sort records by key and sum each run exactly */
     qsort(c->recs, c->nrec, sizeof(rec_t), cmp_rec);
     uint64_t V = 0;
@@ -1376,7 +1376,15 @@ int orc_build(orc_ctx* c, int levels) {
         }
     }
     c->built = 0;
-    for (int l = 1; l <= levels; l++) {
+    return build_up(c, levels);
+}
+
+/* Levels c->built + 1 .. levels from level c->built (P:364 sums, P:376-387 SGGX-H). */
+static int build_up(orc_ctx* c, int levels) {
+    const int K = c->K;
+    float theta[32][3], coef[32][6];
+    theta_table(theta, coef);
+    for (int l = c->built + 1; l <= levels; l++) {
         level_t* Cc = &c->lv[l - 1];
         level_t* P = &c->lv[l];
         uint64_t nP = 0;
@@ -1418,6 +1426,43 @@ int orc_build(orc_ctx* c, int levels) {
         c->built = l;
     }
     return ORC_OK;
+}
+
+/* Test infrastructure: start the pyramid from given records of level l0 (sorted keys, exact
+ * accumulators acc [n][7], lobe counts ncl [n] and lobe accumulators clacc [n][K][7]; for
+ * l0 = 0 ncl / clacc are ignored and derived from acc as in orc_build) and build levels
+ * l0 + 1 .. levels with the same code as orc_build. Lets a test check the upper levels of a
+ * workload too large for the oracle's voxelization against the GPU's records of level l0. */
+int orc_build_from(orc_ctx* c, int l0, uint64_t n, const uint64_t* key, const int64_t* acc, const uint8_t* ncl,
+                   const int64_t* clacc, int levels) {
+    if (l0 < 0 || l0 > levels || levels > c->logN) return ORC_ERR_LEVEL;
+    free_levels(c);
+    const int K = c->K;
+    level_t* L = &c->lv[l0];
+    L->n = n;
+    L->key = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    L->acc = (i128*)calloc((n ? n : 1) * 7, sizeof(i128));
+    L->ncl = (uint8_t*)calloc(n ? n : 1, 1);
+    L->cl = (i128*)calloc((n ? n : 1) * K * 7, sizeof(i128));
+    if (!L->key || !L->acc || !L->ncl || !L->cl) return ORC_ERR_OOM;
+    for (uint64_t x = 0; x < n; x++) {
+        if (x > 0 && key[x] <= key[x - 1]) return ORC_ERR_ARG;
+        L->key[x] = key[x];
+        for (int e = 0; e < 7; e++) L->acc[7 * x + e] = acc[7 * x + e];
+        if (l0 == 0) {
+            if (acc[7 * x] > 0) {
+                L->ncl[x] = 1;
+                for (int e = 0; e < 7; e++) L->cl[(size_t)x * K * 7 + e] = acc[7 * x + e];
+            }
+        } else {
+            if (ncl[x] > K) return ORC_ERR_ARG;
+            L->ncl[x] = ncl[x];
+            for (int q = 0; q < ncl[x]; q++)
+                for (int e = 0; e < 7; e++) L->cl[((size_t)x * K + q) * 7 + e] = clacc[((size_t)x * K + q) * 7 + e];
+        }
+    }
+    c->built = l0;
+    return build_up(c, levels);
 }
 
 uint64_t orc_level_size(const orc_ctx* c, int l) {

@@ -121,8 +121,14 @@ __global__ void k_lod_prep(const long long* __restrict__ cacc,
 // Same arithmetic as k_lod_prep (exact integer sums). The copy is 16-byte aligned by starting
 // up to one 8-byte word early and rounding the size up; every device buffer carries >= 64 B of
 // allocation slack (dalloc), so the rounded tail stays inside the allocation.
-constexpr int PREP_WARPS = 4;
-constexpr int PREP_PAR = 16;                          // parents per warp-iteration
+#ifndef PREP_WARPS_N
+#define PREP_WARPS_N 4
+#endif
+#ifndef PREP_PAR_N
+#define PREP_PAR_N 16
+#endif
+constexpr int PREP_WARPS = PREP_WARPS_N;
+constexpr int PREP_PAR = PREP_PAR_N;                  // parents per warp-iteration
 constexpr int PREP_ROWW = 8 * PREP_PAR * 7 + 2;       // staged words per buffer (+ alignment)
 constexpr int PREP_WARP_WORDS = 2 * PREP_ROWW + PREP_PAR * 7 + 2;   // + acc staging; lobes added per K
 
@@ -996,9 +1002,16 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     timer_begin(c, c->t_prep);
     if (leaf) {
         uint64_t pb = ((V + PREP_PAR - 1) / PREP_PAR + PREP_WARPS - 1) / PREP_WARPS;
-        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), 148ull * 3);
         const size_t psm = (size_t)PREP_WARPS * (PREP_WARP_WORDS + PREP_PAR * K * 7) * sizeof(long long);
-        CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        static int occ[VOX_MAX_K + 1] = {};   // resident blocks per SM (shared memory bound)
+        if (!occ[K]) {
+            CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[K], k_lod_prep_leaf<K>, PREP_WARPS * 32, psm));
+            if (occ[K] < 1) occ[K] = 1;
+        }
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), (uint64_t)nsm * occ[K]);
         k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.acc, start, V, P.acc, P.ncl,
                                                                             P.clacc, nlob, hist);
     } else {

@@ -1,14 +1,17 @@
 """Parity at BASELINE.json's full sizes, in bench.py's launch configuration, on sampled
 outputs: the GPU builds the whole config; the oracle recomputes whole Morton cells (every
 primitive touching a cell, LoD inside it) and every level <= the cell level is compared
-bit-for-bit inside those cells (windowed parity)."""
+bit-for-bit inside those cells (windowed parity). The levels above the
+window are chained: the oracle starts from the GPU's records of a middle level (whose own
+values the windows and the exact conservation sums check) and builds every level above it
+with its own arithmetic, compared bit-for-bit over the whole level."""
 import numpy as np
 import pytest
 import torch
 
 import gen
 import oracle
-from windowing import window_oracle
+from windowing import chain_levels, window_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -60,6 +63,7 @@ def test_config4_fullsize_windowed(P):
     for l in range(1, c["levels"] + 1):
         assert torch.equal(v.level(l)["acc"].sum(0), tot)
     _check(v, c, 6, _cells(k0, 6, 4, np.random.default_rng(0)))
+    chain_levels(v, c, 3)   # levels 4..12 over the whole grid (332k .. 1 voxels)
 
 
 def test_config3_fullsize_windowed(P):

@@ -9,6 +9,7 @@ import torch
 
 import gen
 import oracle
+from windowing import chain_levels
 
 pytestmark = pytest.mark.gpu
 
@@ -75,7 +76,7 @@ def test_hist_config4_windowed(P):
     c = gen.config(4)
     v = P.Vox(c["grid_res"], c["bbox"], distance="hist")
     v.voxelize_fibers(torch.from_numpy(c["segments"]).cuda(), torch.from_numpy(c["radii"]).cuda())
-    v.build_lod(4)
+    v.build_lod(c["levels"])
     k0 = v.level(0)["key"].cpu().numpy().astype(np.uint64)
     cells, cnt = np.unique(k0 >> np.uint64(12), return_counts=True)
     cell = int(cells[np.argsort(-cnt)[len(cnt) // 3]])
@@ -100,3 +101,4 @@ def test_hist_config4_windowed(P):
             assert np.array_equal(g["ncl"][m].cpu().numpy(), rr["ncl"]), l
             assert np.array_equal(g["cl"][m].cpu().numpy(), rr["cl"]), l
     assert int((o.level(1)["ncl"] == 3).sum()) > 50      # the window holds real SGGX-H work
+    chain_levels(v, c, 6)   # levels 7..12 over the whole grid, the oracle from the GPU's level 6

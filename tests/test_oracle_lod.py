@@ -7,6 +7,7 @@ import os
 import numpy as np
 import pytest
 
+import gen
 import oracle
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
@@ -198,3 +199,34 @@ def test_naive_aggregate_delta_x_delta_y():
     assert np.allclose(S, GOLD["interpolate_delta_xy"]["S_expected"], atol=1e-6)
     # SGGX-H with K=3 keeps both lobes (n = 2 <= K), strictly less isotropic than the naive S
     assert L1["ncl"][L1["key"] == (oracle.morton(10, 20, 20) >> 3)][0] == 2
+
+
+def test_build_from_equals_build():
+    """orc_build_from (chained parity at full size) starts from given level records and must
+    reproduce build() exactly: config 1 and a small weave, from every start level, both
+    distance modes."""
+    c = gen.config(1)
+    for distance in ("sigma", "hist"):
+        o = oracle.Oracle(c["grid_res"], c["bbox"], distance=distance, hist_samples=200)
+        o.add_triangles(c["tris"])
+        o.build(6)
+        for l0 in range(0, 6):
+            L = o.level(l0)
+            o2 = oracle.Oracle(c["grid_res"], c["bbox"], distance=distance, hist_samples=200)
+            o2.build_from(l0, L["key"], L["acc"], L["ncl"], L["cl_acc"], 6)
+            for l in range(l0, 7):
+                a, b = o.level(l), o2.level(l)
+                for f in ("key", "acc", "ncl", "cl_acc", "cl"):
+                    assert np.array_equal(a[f], b[f]), (distance, l0, l, f)
+    s, r = gen.plain_weave(n_warp=8, n_weft=8, n_seg=16, pitch=1 / 8)
+    o = oracle.Oracle(64, np.array([0, 0, 0, 1, 1, 1], np.float32))
+    o.add_fibers(s, r)
+    o.build(6)
+    L = o.level(2)
+    o2 = oracle.Oracle(64, np.array([0, 0, 0, 1, 1, 1], np.float32))
+    o2.build_from(2, L["key"], L["acc"], L["ncl"], L["cl_acc"], 6)
+    for l in range(2, 7):
+        assert np.array_equal(o.level(l)["cl_acc"], o2.level(l)["cl_acc"]), l
+    # unsorted keys are rejected
+    with pytest.raises(oracle.OracleError):
+        o2.build_from(2, L["key"][::-1].copy(), L["acc"][::-1].copy(), L["ncl"], L["cl_acc"], 6)

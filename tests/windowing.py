@@ -27,3 +27,20 @@ def window_oracle(c, level, cell, **okw):
         o.add_triangles(np.ascontiguousarray(t[sel]), d)
     o.build(level)
     return o
+
+
+def chain_levels(v, c, l0, k=3, hist_samples=5000):
+    """Oracle levels l0+1..top from the GPU's level-l0 records vs the GPU's own levels."""
+    rec = v.export_level(l0).cpu().numpy().view(np.int64)
+    words = 9 + 7 * k
+    rec = rec.reshape(-1, words)
+    o = oracle.Oracle(c["grid_res"], c["bbox"], k, distance=v.distance, hist_samples=hist_samples)
+    o.build_from(l0, rec[:, 0].view(np.uint64), rec[:, 1:8], rec[:, 8].astype(np.uint8),
+                 rec[:, 9:].reshape(-1, k, 7), c["levels"])
+    for l in range(l0 + 1, c["levels"] + 1):
+        g, r = v.level(l, device="cpu"), o.level(l)
+        assert np.array_equal(g["key"].numpy().astype(np.uint64), r["key"]), (l, "keys")
+        assert np.array_equal(g["acc"].numpy(), r["acc"]), (l, "acc")
+        assert np.array_equal(g["ncl"].numpy(), r["ncl"]), (l, "ncl")
+        assert np.array_equal(g["cl"].numpy(), r["cl"]), (l, "lobes")
+    o.close()
