@@ -199,6 +199,15 @@ __device__ __forceinline__ void far_consts(const float* w, float rg, float& iww,
 // ---------------------------------------------------------------- emit
 
 constexpr int EMIT_WARPS = 8;
+
+// x / d for x < 2^24 (a segment has at most 2^24 candidates, §3) with m = floor((2^32-1)/d):
+// umulhi(x, m) is floor(x/d) or one less (the error x (1 + d) / (d 2^32) < 2^-7), and the
+// remainder test corrects it -- exact, without the integer-division sequence.
+__device__ __forceinline__ uint32_t div_magic(uint32_t x, uint32_t d, uint32_t m) {
+    uint32_t q = __umulhi(x, m);
+    if (x - q * d >= d) q++;
+    return q;
+}
 // Evaluates the first nq (<= 32) queued candidates, one per lane: the pinned predicate and
 // l_r (§4), the exact S_acc contribution (segmented scan over lanes: queue order keeps the
 // owner segments non-decreasing) and the binned append of in-grid, in-shard keys.
@@ -259,7 +268,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
              unsigned* __restrict__ flags) {
     __shared__ float s_f[EMIT_WARPS][18][32];
     __shared__ int64_t s_u0[EMIT_WARPS][3][32];
-    __shared__ uint32_t s_ex[EMIT_WARPS][2][32];
+    __shared__ uint32_t s_ex[EMIT_WARPS][4][32];   // x / y extents and their division magics
     __shared__ uint32_t s_start[EMIT_WARPS][32];
     __shared__ unsigned long long s_acc[EMIT_WARPS][32];
     __shared__ int4 s_q[EMIT_WARPS][64];   // survivor FIFO: (segment lane, i, j, k)
@@ -285,6 +294,8 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                 for (int ax = 0; ax < 3; ax++) s_u0[wib][ax][lane] = G.u0[ax];
                 s_ex[wib][0][lane] = (uint32_t)(G.u1[0] - G.u0[0] + 1);
                 s_ex[wib][1][lane] = (uint32_t)(G.u1[1] - G.u0[1] + 1);
+                s_ex[wib][2][lane] = 0xffffffffu / s_ex[wib][0][lane];
+                s_ex[wib][3][lane] = 0xffffffffu / s_ex[wib][1][lane];
             }
             f.moving = 0;
             for (int ax = 0; ax < 3; ax++) {
@@ -335,10 +346,11 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
                     if (s_start[wib][o + step] <= c) o += step;
                 const uint32_t local = c - s_start[wib][o];
                 const uint32_t ex = s_ex[wib][0][o], ey = s_ex[wib][1][o];
-                const uint32_t t = local / ex;
+                const uint32_t t = div_magic(local, ex, s_ex[wib][2][o]);
+                const uint32_t tk = div_magic(t, ey, s_ex[wib][3][o]);
                 const int64_t i = s_u0[wib][0][o] + (int64_t)(local - t * ex);
-                const int64_t j = s_u0[wib][1][o] + (int64_t)(t % ey);
-                const int64_t k = s_u0[wib][2][o] + (int64_t)(t / ey);
+                const int64_t j = s_u0[wib][1][o] + (int64_t)(t - tk * ey);
+                const int64_t k = s_u0[wib][2][o] + (int64_t)tk;
                 float av[3], dv[3];
                 for (int ax = 0; ax < 3; ax++) {
                     av[ax] = s_f[wib][ax][o];
