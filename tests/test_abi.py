@@ -86,3 +86,23 @@ def test_plan_shards_properties(P):
         assert np.array_equal(b, P.plan_shards(w, world))           # deterministic
     b = P.plan_shards(np.zeros(64, np.uint64), 4)
     assert list(b) == [0, 16, 32, 48, 64]
+
+
+def test_release_debug_flags_zero(P):
+    # the bounds checks exist only in the -DVOX_DEBUG build; the release library reports none
+    f = C.c_uint32(7)
+    assert P.lib().vox_debug_flags(C.byref(f)) == 0 and f.value == 0
+
+
+def test_no_contracted_packed_fma_in_sass(P):
+    """The pinned sequences forbid FMA contraction (-fmad=false). ptxas contracts packed
+    mul.f32x2 + add.f32x2 into FFMA2 even then, so the shipped SASS must hold no
+    FFMA2 at all."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([exe, "-sass", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "Function :" in sass
+    assert "FFMA2" not in sass
