@@ -200,7 +200,8 @@ vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_
  * clustering of level l and the build of levels > l. Building further levels does not touch
  * lower levels; the caller synchronises `stream` before reading the buffers or destroying
  * the ctx. The fp32 values are formed from the accumulators by a small kernel on `stream`
- * into stream-ordered scratch (freed on `stream`; vox_trim releases it) before each D2H.
+ * into stream-ordered scratch from the device pool (allocated and freed on `stream`) before
+ * each D2H; a level whose views an earlier read formed is copied from them, after that read.
  * Level 0 supports key / mass / m6 only (ncl or cl non-NULL -> VOX_ERR_INVALID_ARG). */
 vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                                 uint8_t* ncl, float* cl, void* stream);

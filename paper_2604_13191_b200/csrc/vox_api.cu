@@ -41,11 +41,10 @@ static size_t round_bytes(size_t b) {
     return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);   // 2 MiB granularity
 }
 
-cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) { return dalloc_s(c, c->stream, p, bytes); }
-
-// allocation ordered on stream s (the block cache is keyed by stream: a freed block is only
-// handed out again on the stream that used it)
-cudaError_t dalloc_s(vox_ctx* c, cudaStream_t s, void** p, size_t bytes) {
+// stream-ordered allocation on the ctx stream; freed blocks are cached per stream (a block is
+// only handed out again on the stream that used it)
+cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes) {
+    cudaStream_t s = c->stream;
     *p = nullptr;
     const size_t want = round_bytes((bytes ? bytes : 16) + 64);   // >= 64 B slack (bulk-copy tails)
     const auto t0 = std::chrono::steady_clock::now();
@@ -906,22 +905,30 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
         CKS(cudaStreamWaitEvent(s, e0, 0));
         CKS(cudaEventDestroy(e0));
     }
-    // the fp32 views are formed from the accumulators on `s` into stream-ordered scratch
-    // (unless the level already holds them), so the build on the ctx stream is not delayed
+    // the fp32 views are formed from the accumulators on `s` into stream-ordered scratch from
+    // the device pool (cudaMallocAsync / cudaFreeAsync on `s`), unless the level already holds
+    // them, so the build on the ctx stream is not delayed
     const bool have = L.f32;
     if (key) CKS(cudaMemcpyAsync(key, L.key, n * 8, cudaMemcpyDefault, s));
+    if (have && (mass || m6)) {   // views formed by an earlier read: ordered after it
+        cudaEvent_t e1;
+        CKS(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        CKS(cudaEventRecord(e1, c->stream));
+        CKS(cudaStreamWaitEvent(s, e1, 0));
+        CKS(cudaEventDestroy(e1));
+    }
     if (mass || m6) {
         float *tm = have ? L.mass : nullptr, *t6 = have ? L.m6 : nullptr;
         if (!have) {
-            if (mass) CKS(dalloc_s(c, s, (void**)&tm, n * 4));
-            if (m6) CKS(dalloc_s(c, s, (void**)&t6, n * 24));
+            if (mass) CKS(cudaMallocAsync((void**)&tm, n * 4, s));
+            if (m6) CKS(cudaMallocAsync((void**)&t6, n * 24, s));
             CKS(launch_finalize(c, s, n, L.acc, nullptr, nullptr, mass ? tm : nullptr, m6 ? t6 : nullptr, nullptr));
         }
         if (mass) CKS(cudaMemcpyAsync(mass, tm, n * 4, cudaMemcpyDefault, s));
         if (m6) CKS(cudaMemcpyAsync(m6, t6, n * 24, cudaMemcpyDefault, s));
         if (!have) {
-            dfree(c, tm);
-            dfree(c, t6);
+            if (tm) CKS(cudaFreeAsync(tm, s));
+            if (t6) CKS(cudaFreeAsync(t6, s));
         }
     }
     cudaEvent_t ev;
@@ -933,13 +940,12 @@ vox_status vox_copy_level_async(vox_ctx* c, uint32_t level, uint64_t* key, float
     if (cl) {
         float* tc = have ? L.cl : nullptr;
         if (!have) {
-            CKS(dalloc_s(c, s, (void**)&tc, n * c->K * 28));
+            CKS(cudaMallocAsync((void**)&tc, n * c->K * 28, s));
             CKS(launch_finalize(c, s, n, nullptr, L.ncl, L.clacc, nullptr, nullptr, tc));
         }
         CKS(cudaMemcpyAsync(cl, tc, n * c->K * 28, cudaMemcpyDefault, s));
-        if (!have) dfree(c, tc);
+        if (!have) CKS(cudaFreeAsync(tc, s));
     }
-    if (s != c->stream) c->aux_streams.insert(s);
     // the level's arrays are being read on `s` until here: free_level / import wait on it
     if (!c->ev_read[level]) CKS(cudaEventCreateWithFlags(&c->ev_read[level], cudaEventDisableTiming));
     CKS(cudaEventRecord(c->ev_read[level], s));
@@ -1074,11 +1080,6 @@ vox_status vox_trim(vox_ctx* c) {
     if (!c) return VOX_ERR_INVALID_ARG;
     CKS(ssync(c));
     vox_trim_stream(c->stream);
-    for (cudaStream_t s : c->aux_streams) {   // scratch of async copies, cached per stream
-        CKS(cudaStreamSynchronize(s));
-        vox_trim_stream(s);
-        CKS(cudaStreamSynchronize(s));
-    }
     CKS(ssync(c));
     return VOX_OK;
 }

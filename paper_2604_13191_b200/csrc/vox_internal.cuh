@@ -9,7 +9,6 @@
 #include <stdint.h>
 
 #include <initializer_list>
-#include <set>
 #include <string>
 #include <vector>
 
@@ -243,7 +242,6 @@ struct vox_ctx {
     cudaEvent_t ev_read[VOX_MAX_LEVELS] = {};
     bool ev_read_pending[VOX_MAX_LEVELS] = {};
     int dev = 0;                            // device of the ctx (event pool key)
-    std::set<cudaStream_t> aux_streams;     // caller streams that received async-copy scratch
     void* h_map = nullptr;                  // host-mapped pinned block for small readbacks
     void* d_map = nullptr;                  // its device alias
     int samp_n = 0;                         // samples per piece / triangle budget of the call (§12)
@@ -260,7 +258,6 @@ namespace vox {
 
 // allocation helpers (stream-ordered)
 cudaError_t dalloc(vox_ctx* c, void** p, size_t bytes);
-cudaError_t dalloc_s(vox_ctx* c, cudaStream_t s, void** p, size_t bytes);   // ordered on stream s
 cudaError_t ssync(vox_ctx* c);   // cudaStreamSynchronize with host-time accounting
 struct ReadItem {
     void* dst;

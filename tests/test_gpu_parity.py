@@ -167,6 +167,18 @@ def test_host_entry_points(P):
     for l in (0, 3):
         assert int(w.view(l)["n"]) == w.size(l)
         _cmp_level(w.level(l, device="cpu"), o.level(l), l, "view")
+    # an async copy of a level whose views a read formed copies those views, after the read
+    n3 = w.size(3)
+    again = {"key": torch.empty(n3, dtype=torch.int64).pin_memory(),
+             "mass": torch.empty(n3, dtype=torch.float32).pin_memory(),
+             "m6": torch.empty((n3, 6), dtype=torch.float32).pin_memory(),
+             "ncl": torch.empty(n3, dtype=torch.uint8).pin_memory(),
+             "cl": torch.empty((n3, 3, 7), dtype=torch.float32).pin_memory()}
+    w.copy_level_async(3, again, side)
+    side.synchronize()
+    r = o.level(3)
+    assert np.array_equal(again["mass"].numpy(), r["mass"]) and np.array_equal(again["m6"].numpy(), r["m6"])
+    assert np.array_equal(again["cl"].numpy(), r["cl"])
     for l in range(1, 7):
         r = o.level(l)
         assert np.array_equal(outs[l]["key"].numpy().astype(np.uint64), r["key"])
