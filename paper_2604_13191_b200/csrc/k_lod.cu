@@ -1003,15 +1003,20 @@ static vox_status run_level(vox_ctx* c, const Level& C, int leaf, const uint32_t
     if (leaf) {
         uint64_t pb = ((V + PREP_PAR - 1) / PREP_PAR + PREP_WARPS - 1) / PREP_WARPS;
         const size_t psm = (size_t)PREP_WARPS * (PREP_WARP_WORDS + PREP_PAR * K * 7) * sizeof(long long);
-        static int occ[VOX_MAX_K + 1] = {};   // resident blocks per SM (shared memory bound)
-        if (!occ[K]) {
-            CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[K], k_lod_prep_leaf<K>, PREP_WARPS * 32, psm));
-            if (occ[K] < 1) occ[K] = 1;
-        }
+        CK(cudaFuncSetAttribute(k_lod_prep_leaf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        // resident blocks per SM (shared memory bound), once per K (thread-safe static init)
+        static const int occ = [psm]() {
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_lod_prep_leaf<K>, PREP_WARPS * 32, psm) !=
+                cudaSuccess) {
+                cudaGetLastError();
+                o = 3;
+            }
+            return o < 1 ? 1 : o;
+        }();
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
-        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), (uint64_t)nsm * occ[K]);
+        pb = std::min<uint64_t>(std::max<uint64_t>(pb, 1), (uint64_t)nsm * occ);
         k_lod_prep_leaf<K><<<(unsigned)pb, PREP_WARPS * 32, psm, c->stream>>>(C.acc, start, V, P.acc, P.ncl,
                                                                             P.clacc, nlob, hist);
     } else {
