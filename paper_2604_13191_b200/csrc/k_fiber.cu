@@ -435,13 +435,22 @@ __device__ __forceinline__ void fib_setup(Fib& f, float (&d)[3], const float* a,
 // 512 sub-voxels, 16 per lane: the §4 predicate on the 8x grid, with conservative shortcuts
 // (centre farther than R + sqrt(3)/2 + 0.1 fine voxels: no hit; the box within R - 0.1 of
 // the segment point nearest its centre: hit) that the pinned fp32 decision cannot contradict (its deviation
-// from the exact one is < 0.02 fine voxels at 8N <= 65536). The mask of each key voxel is
-// OR-ed into the level-0 masks (a key absent from level 0 = another shard: skipped).
+// from the exact one is < 0.02 fine voxels at 8N <= 65536). The undecided sub-voxels of the
+// segment's key voxels (about 16 per voxel) go to one per-warp ring and are evaluated 32 at a
+// time across voxels, so the pinned predicate runs on full warps; up to DENS_PV key voxels are
+// pending, each with its mask in shared memory, and their masks are OR-ed into the level-0
+// masks when the pending set is full or the segment ends (a key absent from level 0 = another
+// shard: skipped).
+constexpr int DENS_PV = 32;          // pending key voxels per warp
+constexpr int DENS_RING = 1024;     // undecided entries per warp (>= 31 + 512 live at once)
+
 __global__ void __launch_bounds__(256, 2)
 k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, uint64_t S, GridXf g,
                 const uint64_t* __restrict__ keys0, uint64_t n0, unsigned long long* __restrict__ masks) {
-    __shared__ unsigned s_m[8][16];        // per warp: the voxel's 512-bit mask
-    __shared__ uint16_t s_q[8][512];       // per warp: undecided sub-voxels
+    __shared__ unsigned s_m[8][DENS_PV][16];   // per warp: the pending voxels' 512-bit masks
+    __shared__ long long s_vidx[8][DENS_PV];   // their level-0 indices
+    __shared__ int s_vc[8][DENS_PV][3];        // their voxel coordinates
+    __shared__ uint16_t s_q[8][DENS_RING];     // per warp: undecided (slot << 9 | sub), a ring
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarp = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -468,29 +477,47 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
         const float far2 = far * far, near2 = near > 0.0f ? near * near : -1.0f;
         const int64_t ex = G.e1[0] - G.e0[0] + 1, ey = G.e1[1] - G.e0[1] + 1, ez = G.e1[2] - G.e0[2] + 1;
         const int64_t ncand = ex * ey * ez;
-        for (int64_t base = 0; base < ncand; base += 32) {
-            const int64_t cidx = base + lane;
-            int64_t i = 0, j = 0, k = 0;
-            bool key = false;
-            if (cidx < ncand) {
-                i = G.e0[0] + cidx % ex;
-                j = G.e0[1] + (cidx / ex) % ey;
-                k = G.e0[2] + cidx / (ex * ey);
-                float ell;
-                key = !far_from_capsule(f.a, d, iww, thr2, i, j, k) && fiber_key(f, i, j, k, ell);
+        int pv = 0;                    // pending voxels
+        unsigned head = 0, tail = 0;   // ring of undecided entries [head, tail)
+        int64_t base = 0, i = 0, j = 0, k = 0;
+        long long my_idx = -1;
+        unsigned bal = 0;
+        // one loop with a single evaluation site (the pinned predicate is inlined only once):
+        // take the next key voxel of the segment, classify its sub-voxels, evaluate full rounds of
+        // undecided ones; when the pending set is full or the segment is done, evaluate the rest
+        // and OR the pending masks into level 0
+        for (;;) {
+            while (bal == 0 && base < ncand) {   // next chunk of candidates with key voxels
+                const int64_t cidx = base + lane;
+                bool key = false;
+                if (cidx < ncand) {
+                    i = G.e0[0] + cidx % ex;
+                    j = G.e0[1] + (cidx / ex) % ey;
+                    k = G.e0[2] + cidx / (ex * ey);
+                    float ell;
+                    key = !far_from_capsule(f.a, d, iww, thr2, i, j, k) && fiber_key(f, i, j, k, ell);
+                }
+                // every key lane searches its leaf at once (the searches' load latencies overlap)
+                my_idx = key ? find_key(keys0, n0, morton3((uint32_t)i, (uint32_t)j, (uint32_t)k)) : -1;
+                bal = __ballot_sync(0xffffffffu, my_idx >= 0);
+                base += 32;
             }
-            // every key lane searches its leaf at once (the searches' load latencies overlap)
-            const long long my_idx = key ? find_key(keys0, n0, morton3((uint32_t)i, (uint32_t)j, (uint32_t)k)) : -1;
-            unsigned bal = __ballot_sync(0xffffffffu, my_idx >= 0);
-            while (bal) {
+            const bool done = bal == 0;
+            if (!done) {
                 const int src = __ffs(bal) - 1;
                 bal &= bal - 1;
                 const int64_t vi = __shfl_sync(0xffffffffu, i, src), vj = __shfl_sync(0xffffffffu, j, src),
                               vk = __shfl_sync(0xffffffffu, k, src);
                 const long long idx = __shfl_sync(0xffffffffu, my_idx, src);
+                const int slot = pv++;
+                if (lane == 0) {
+                    s_vidx[wib][slot] = idx;
+                    s_vc[wib][slot][0] = (int)vi;
+                    s_vc[wib][slot][1] = (int)vj;
+                    s_vc[wib][slot][2] = (int)vk;
+                }
                 // classify the 512 sub-voxels (16 per lane): sure hits straight into the mask,
-                // undecided ones queued, then the queue evaluated 32 at a time (no divergence)
-                int nq = 0;
+                // undecided ones queued
                 // c2 = squared distance of the sub-voxel centre to the segment, box2 = squared
                 // distance of the segment point nearest that centre to the sub-voxel box: the
                 // segment-box distance lies in [sqrt(c2) - sqrt(3)/2, sqrt(box2)].
@@ -516,28 +543,40 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                     const bool sure = box2 < near2, open = !sure && !(c2 > far2);
                     const unsigned bs = __ballot_sync(0xffffffffu, sure);
                     const unsigned bo = __ballot_sync(0xffffffffu, open);
-                    if (lane == 0) s_m[wib][q] = bs;
-                    if (open) s_q[wib][nq + __popc(bo & ((1u << lane) - 1u))] = (uint16_t)sub;
-                    nq += __popc(bo);
-                }
-                __syncwarp();
-#pragma unroll 1
-                for (int b0 = 0; b0 < nq; b0 += 32) {
-                    if (b0 + lane < nq) {
-                        const int sub = s_q[wib][b0 + lane];
-                        float ell;
-                        if (fiber_key(f8, 8 * vi + (sub & 7), 8 * vj + ((sub >> 3) & 7), 8 * vk + (sub >> 6), ell))
-                            atomicOr(&s_m[wib][sub >> 5], 1u << (sub & 31));
-                    }
-                }
-                __syncwarp();
-                if (lane < 8) {
-                    const unsigned long long word =
-                        (unsigned long long)s_m[wib][2 * lane] | ((unsigned long long)s_m[wib][2 * lane + 1] << 32);
-                    if (word) atomicOr(&masks[8 * idx + lane], word);
+                    if (lane == 0) s_m[wib][slot][q] = bs;
+                    if (open)
+                        s_q[wib][(tail + __popc(bo & ((1u << lane) - 1u))) & (DENS_RING - 1)] =
+                            (uint16_t)((slot << 9) | sub);
+                    tail += __popc(bo);
                 }
                 __syncwarp();
             }
+            const bool full = done || pv == DENS_PV;
+            while (tail - head >= 32u || (full && head != tail)) {   // the one evaluation site
+                const unsigned cnt = tail - head < 32u ? tail - head : 32u;
+                if ((unsigned)lane < cnt) {
+                    const unsigned e = s_q[wib][(head + lane) & (DENS_RING - 1)];
+                    const int slot = e >> 9, sub = e & 511;
+                    float ell;
+                    if (fiber_key(f8, 8 * (int64_t)s_vc[wib][slot][0] + (sub & 7),
+                                  8 * (int64_t)s_vc[wib][slot][1] + ((sub >> 3) & 7),
+                                  8 * (int64_t)s_vc[wib][slot][2] + (sub >> 6), ell))
+                        atomicOr(&s_m[wib][slot][sub >> 5], 1u << (sub & 31));
+                }
+                head += cnt;
+                __syncwarp();
+            }
+            if (full) {
+                for (int w = lane; w < pv * 8; w += 32) {
+                    const int slot = w >> 3, q = w & 7;
+                    const unsigned long long word = (unsigned long long)s_m[wib][slot][2 * q] |
+                                                    ((unsigned long long)s_m[wib][slot][2 * q + 1] << 32);
+                    if (word) atomicOr(&masks[8 * s_vidx[wib][slot] + q], word);
+                }
+                pv = 0;
+                __syncwarp();
+            }
+            if (done) break;
         }
     }
 }
