@@ -528,18 +528,21 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                 const float e1a = (((float)(8 * vj) + 0.5f) - f8.a[1]) + (float)(lane >> 3);
                 const float e1b = e1a + 4.0f;
                 const float e2b = ((float)(8 * vk) + 0.5f) - f8.a[2];
-                const float pa = e0 * d8[0] + e1a * d8[1], pb = e0 * d8[0] + e1b * d8[1];
+                // (this classifier is conservative geometry, not the pinned predicate: fused
+                // multiply-adds are fine here, their rounding is far inside the 0.1 margin)
+                const float pa = __fmaf_rn(e1a, d8[1], e0 * d8[0]), pb = __fmaf_rn(e1b, d8[1], e0 * d8[0]);
 #pragma unroll 1
                 for (int q = 0; q < 16; q++) {
                     const int sub = lane + 32 * q;
                     const float e1 = (q & 1) ? e1b : e1a, e2 = e2b + (float)(q >> 1);
-                    float t = (((q & 1) ? pb : pa) + e2 * d8[2]) * iww8;
-                    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
-                    const float q0 = e0 - t * d8[0], q1 = e1 - t * d8[1], q2 = e2 - t * d8[2];
+                    float t = __fmaf_rn(e2, d8[2], (q & 1) ? pb : pa) * iww8;
+                    t = fminf(fmaxf(t, 0.0f), 1.0f);
+                    const float q0 = __fmaf_rn(-t, d8[0], e0), q1 = __fmaf_rn(-t, d8[1], e1),
+                                q2 = __fmaf_rn(-t, d8[2], e2);
                     const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f),
                                 o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
-                    const float box2 = o0 * o0 + o1 * o1 + o2 * o2;
-                    const float c2 = q0 * q0 + q1 * q1 + q2 * q2;
+                    const float box2 = __fmaf_rn(o0, o0, __fmaf_rn(o1, o1, o2 * o2));
+                    const float c2 = __fmaf_rn(q0, q0, __fmaf_rn(q1, q1, q2 * q2));
                     const bool sure = box2 < near2, open = !sure && !(c2 > far2);
                     const unsigned bs = __ballot_sync(0xffffffffu, sure);
                     const unsigned bo = __ballot_sync(0xffffffffu, open);
