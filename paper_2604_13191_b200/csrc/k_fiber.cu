@@ -180,11 +180,12 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
 // compare the emitted key sets with the oracle, which has no such shortcut.
 __device__ __forceinline__ bool far_from_capsule(const float* a, const float* d, float iww, float thr2, int64_t i,
                                                  int64_t j, int64_t k) {
+    // conservative geometry (not the pinned predicate): fused multiply-adds are fine here
     const float e0 = ((float)i + 0.5f) - a[0], e1 = ((float)j + 0.5f) - a[1], e2 = ((float)k + 0.5f) - a[2];
-    float t = (e0 * d[0] + e1 * d[1] + e2 * d[2]) * iww;   // iww = 1 / |d|^2 (0 for a sphere)
-    t = t < 0.0f ? 0.0f : (t > 1.0f ? 1.0f : t);
-    const float q0 = e0 - t * d[0], q1 = e1 - t * d[1], q2 = e2 - t * d[2];
-    return q0 * q0 + q1 * q1 + q2 * q2 > thr2;
+    float t = __fmaf_rn(e2, d[2], __fmaf_rn(e1, d[1], e0 * d[0])) * iww;   // iww = 1 / |d|^2 (0 for a sphere)
+    t = fminf(fmaxf(t, 0.0f), 1.0f);
+    const float q0 = __fmaf_rn(-t, d[0], e0), q1 = __fmaf_rn(-t, d[1], e1), q2 = __fmaf_rn(-t, d[2], e2);
+    return __fmaf_rn(q0, q0, __fmaf_rn(q1, q1, q2 * q2)) > thr2;
 }
 // the per-segment constants of far_from_capsule: 1 / |d|^2 and (rg + sqrt(3)/2 + 0.05)^2. A
 // rounded t only moves the nearest point along the segment, which changes the distance by
