@@ -367,14 +367,17 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             }
             qn += __popc(bal);
             __syncwarp();
-            if (qn >= 32) {
-                eval_queue(s_q[wib], 32, lane, s_f[wib], s_acc[wib], batch, g, sh, bins, keys, vals, flags);
-                if (lane < qn - 32) s_q[wib][lane] = s_q[wib][32 + lane];
-                qn -= 32;
+            // the one evaluation site (the pinned predicate is inlined once): full rounds, and
+            // after the last chunk the rest
+            const bool last = c0 + 32 >= total;
+            while (qn >= 32 || (last && qn > 0)) {
+                const int m = qn < 32 ? qn : 32;
+                eval_queue(s_q[wib], m, lane, s_f[wib], s_acc[wib], batch, g, sh, bins, keys, vals, flags);
+                if (lane < qn - m) s_q[wib][lane] = s_q[wib][m + lane];
+                qn -= m;
                 __syncwarp();
             }
         }
-        if (qn) eval_queue(s_q[wib], qn, lane, s_f[wib], s_acc[wib], batch, g, sh, bins, keys, vals, flags);
         __syncwarp();
         if (p < S) {
             // §5 per-segment normalisation f_p = m_p / S_p and unit tangent
