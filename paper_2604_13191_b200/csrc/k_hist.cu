@@ -64,7 +64,9 @@ __device__ __forceinline__ int hist_bin1(float d) {
 }
 
 // histogram of the lobe (w, M6) accumulators `lob` into H[0..124]; priv: 1000 words scratch
-__device__ __forceinline__ void hist_build(const long long* lob, const float* __restrict__ ux,
+// not inlined: called at two sites (initial lobes, merged lobe), each call is thousands of
+// instructions, so one copy of the code keeps the kernel's hot loops in the instruction cache
+__device__ __noinline__ void hist_build(const long long* lob, const float* __restrict__ ux,
                                            const float* __restrict__ uy, const float* __restrict__ uz, int N,
                                            uint32_t* priv, uint16_t* H, int lane) {
     for (int w = lane; w < HB * 8; w += 32) priv[w] = 0u;
@@ -182,7 +184,8 @@ __device__ __forceinline__ void hist_pairs(const uint16_t* Hi, const uint16_t* c
 }
 
 // distances of row i to the listed columns xs[0..m-1] (m <= 4), batched
-__device__ __forceinline__ void hist_row4(const uint16_t (*H)[128], int i, const int (&xs)[4], int m,
+// not inlined (two call sites, as hist_build)
+__device__ __noinline__ void hist_row4(const uint16_t (*H)[128], int i, const int (&xs)[4], int m,
                                           const uint32_t* __restrict__ pg, int lane,
                                           unsigned long long (&out)[4]) {
     const uint16_t* Hj[4] = {H[xs[0]], H[xs[m > 1 ? 1 : 0]], H[xs[m > 2 ? 2 : 0]], H[xs[m > 3 ? 3 : 0]]};
