@@ -375,7 +375,7 @@ __device__ __forceinline__ int gather_lobes(const uint32_t* __restrict__ start, 
 // a shared 28-entry table per parent; the lexicographic argmin (d, i, j) is a group reduce.
 constexpr int QUAD_WARPS = 4;
 #ifndef QUAD_MINB
-#define QUAD_MINB 6
+#define QUAD_MINB 7
 #endif
 
 __device__ __forceinline__ float part4(const float* a, const float* b) {
@@ -405,6 +405,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     __shared__ long long s_lobe[QUAD_WARPS][4][8][7];
     __shared__ __align__(16) float s_S[QUAD_WARPS][4][8][6];
     __shared__ float s_D[QUAD_WARPS][4][28];
+    __shared__ __align__(16) float4 s_sg[QUAD_WARPS][4][8][8];   // [group][lobe][lane]: the lane's 4 slices
     __shared__ uint16_t s_pair[28];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int l = lane & 7, g = lane >> 3;
@@ -490,15 +491,12 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             for (int e = 0; e < 6; e++) Sg[l][e] = deq32(lobe[l][1 + e]) / wf;
         }
         __syncwarp();
-        float sg[8][4];
-#pragma unroll
-        for (int c = 0; c < 8; c++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) sg[c][q] = 0.0f;
+        // the lane's 4 sigma slices of every lobe live in shared memory (its own float4 per
+        // lobe: conflict-free), so the loops need no unrolling over lobes and no registers
+        float4(*sg4)[8] = s_sg[wib][g];
         // lobe-outer: each lobe's S row is read once and used for the lane's 4 slices
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            if (c >= nmax) break;
+#pragma unroll 1
+        for (int c = 0; c < nmax; c++) {
             float2 s01 = make_float2(0.0f, 0.0f), s23 = s01, s45 = s01;
             if (valid && c < n) {
                 const float2* sr = reinterpret_cast<const float2*>(Sg[c]);
@@ -506,6 +504,7 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 s23 = sr[1];
                 s45 = sr[2];
             }
+            float sq[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 float qq = cf[q][0].x * s01.x;
@@ -514,15 +513,20 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 qq = qq + cf[q][1].y * s23.y;
                 qq = qq + cf[q][2].x * s45.x;
                 qq = qq + cf[q][2].y * s45.y;
-                sg[c][q] = sqrtf(pmax(qq, 0.0f));
+                sq[q] = sqrtf(pmax(qq, 0.0f));
             }
+            sg4[c][l] = make_float4(sq[0], sq[1], sq[2], sq[3]);
         }
-#pragma unroll
-        for (int j = 1; j < 8; j++) {
-            if (j >= nmax) break;
-#pragma unroll
+        __syncwarp();
+#pragma unroll 1
+        for (int j = 1; j < nmax; j++) {
+            const float4 vj = sg4[j][l];
+            const float aj[4] = {vj.x, vj.y, vj.z, vj.w};
+#pragma unroll 1
             for (int i = 0; i < j; i++) {
-                const float s2 = group_sum8(part4(sg[i], sg[j]));
+                const float4 vi = sg4[i][l];
+                const float ai[4] = {vi.x, vi.y, vi.z, vi.w};
+                const float s2 = group_sum8(part4(ai, aj));
                 const int t = j * (j - 1) / 2 + i;
                 if (l == (t & 7)) D[t] = (valid && j < n) ? s2 : __uint_as_float(INF_BITS);
             }
@@ -569,18 +573,15 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
                 qq = qq + cf[q][2].y * m45.y;
                 sn[q] = sqrtf(pmax(qq, 0.0f));
             }
-#pragma unroll
-            for (int c = 0; c < 8; c++)
-                if (act && c == bi) {
-#pragma unroll
-                    for (int q = 0; q < 4; q++) sg[c][q] = sn[q];
-                }
+            if (act) sg4[bi][l] = make_float4(sn[0], sn[1], sn[2], sn[3]);
             if (act) alive &= ~(1u << bj);
+            __syncwarp();
             float mine = 0.0f;
-#pragma unroll
-            for (int x = 0; x < 8; x++) {
-                if (x >= nmax) break;
-                const float v = group_sum8(part4(sn, sg[x]));
+#pragma unroll 1
+            for (int x = 0; x < nmax; x++) {
+                const float4 vx = sg4[x][l];
+                const float ax[4] = {vx.x, vx.y, vx.z, vx.w};
+                const float v = group_sum8(part4(sn, ax));
                 if (l == x) mine = v;
             }
             if (act && l < n) {
