@@ -369,7 +369,7 @@ __device__ __forceinline__ int gather_lobes(const uint32_t* __restrict__ start, 
 
 // ---------------------------------------------------------------- SGGX-H, n <= 8 ("quad")
 // Four parents per warp, eight lanes per parent. Lane l of a group owns slices l, l+8,
-// l+16, l+24 of every lobe's sigma (registers). A distance is formed as the pinned tree
+// l+16, l+24 of every lobe's sigma (a float4 per lobe in shared memory). A distance is formed as the pinned tree
 // pairs it -- s[l] = d[l] + d[l+16], s[l+8] = d[l+8] + d[l+24], s[l] = s[l] + s[l+8] in
 // registers, then the last three tree levels by xor-shuffles inside the group -- and kept in
 // a shared 28-entry table per parent; the lexicographic argmin (d, i, j) is a group reduce.
