@@ -381,11 +381,17 @@ constexpr int QUAD_WARPS = 4;
 __device__ __forceinline__ float part4(const float* a, const float* b) {
     return (fabsf(a[0] - b[0]) + fabsf(a[2] - b[2])) + (fabsf(a[1] - b[1]) + fabsf(a[3] - b[3]));
 }
-__device__ __forceinline__ float group_sum8(float s) {
-    s = s + __shfl_xor_sync(0xffffffffu, s, 4);
-    s = s + __shfl_xor_sync(0xffffffffu, s, 2);
-    s = s + __shfl_xor_sync(0xffffffffu, s, 1);
-    return s;
+// Eight distances at once: slot s of lane l holds the lane's part4 of pair (s ^ l); at step h
+// a lane keeps the slots with bit h clear and adds the partner's slot s | h, which holds the
+// same pair (s ^ l = (s | h) ^ (l ^ h)). Lane l ends with pair l's sum, and each addition is
+// the pinned tree's s[x] + s[x + h] (fp32 addition is commutative): bit-identical to the
+// per-pair xor reduce, with 7 shuffles per 8 pairs instead of 24 and no selects.
+__device__ __forceinline__ float group_sum8x8(float (&v)[8]) {
+#pragma unroll
+    for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+        for (int s = 0; s < h; s++) v[s] = v[s] + __shfl_xor_sync(0xffffffffu, v[s + h], h);
+    return v[0];
 }
 __device__ __forceinline__ unsigned long long group_min8(unsigned long long v) {
 #pragma unroll
@@ -406,13 +412,13 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
     __shared__ __align__(16) float s_S[QUAD_WARPS][4][8][6];
     __shared__ float s_D[QUAD_WARPS][4][28];
     __shared__ __align__(16) float4 s_sg[QUAD_WARPS][4][8][8];   // [group][lobe][lane]: the lane's 4 slices
-    __shared__ uint16_t s_pair[28];
+    __shared__ uint16_t s_pair[32];   // 28 pairs; entries 28..31 pad the last batch of 8
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int l = lane & 7, g = lane >> 3;
-    if (threadIdx.x < 28) {
+    if (threadIdx.x < 32) {
         int j = 1;
         while ((j + 1) * j / 2 <= (int)threadIdx.x) j++;
-        s_pair[threadIdx.x] = (uint16_t)((((int)threadIdx.x - j * (j - 1) / 2) << 8) | j);
+        s_pair[threadIdx.x] = threadIdx.x < 28 ? (uint16_t)((((int)threadIdx.x - j * (j - 1) / 2) << 8) | j) : (uint16_t)1;
     }
     __syncthreads();
     long long(*lobe)[7] = s_lobe[wib][g];
@@ -518,18 +524,21 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             sg4[c][l] = make_float4(sq[0], sq[1], sq[2], sq[3]);
         }
         __syncwarp();
+        // pairs t = 8b + (s ^ l) in slot s of lane l; lane l ends with pair 8b + l
+        const int npq = nmax * (nmax - 1) / 2;
 #pragma unroll 1
-        for (int j = 1; j < nmax; j++) {
-            const float4 vj = sg4[j][l];
-            const float aj[4] = {vj.x, vj.y, vj.z, vj.w};
-#pragma unroll 1
-            for (int i = 0; i < j; i++) {
-                const float4 vi = sg4[i][l];
-                const float ai[4] = {vi.x, vi.y, vi.z, vi.w};
-                const float s2 = group_sum8(part4(ai, aj));
-                const int t = j * (j - 1) / 2 + i;
-                if (l == (t & 7)) D[t] = (valid && j < n) ? s2 : __uint_as_float(INF_BITS);
+        for (int b = 0; b < npq; b += 8) {
+            float v[8];
+#pragma unroll
+            for (int s = 0; s < 8; s++) {
+                const int pr = s_pair[b + (s ^ l)];
+                const float4 vi = sg4[pr >> 8][l], vj = sg4[pr & 0xff][l];
+                const float ai[4] = {vi.x, vi.y, vi.z, vi.w}, aj[4] = {vj.x, vj.y, vj.z, vj.w};
+                v[s] = part4(ai, aj);
             }
+            const float s2 = group_sum8x8(v);
+            const int t = b + l;
+            if (t < npq) D[t] = (valid && (s_pair[t] & 0xff) < n) ? s2 : __uint_as_float(INF_BITS);
         }
         __syncwarp();
         unsigned alive = (1u << n) - 1u;
@@ -576,14 +585,16 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             if (act) sg4[bi][l] = make_float4(sn[0], sn[1], sn[2], sn[3]);
             if (act) alive &= ~(1u << bj);
             __syncwarp();
-            float mine = 0.0f;
-#pragma unroll 1
-            for (int x = 0; x < nmax; x++) {
-                const float4 vx = sg4[x][l];
+            // d(bi, x) for x = 0..7 at once: slot s of lane l holds x = s ^ l (rows >= n are
+            // never used: their sums land only in lanes >= n)
+            float v[8];
+#pragma unroll
+            for (int s = 0; s < 8; s++) {
+                const float4 vx = sg4[s ^ l][l];
                 const float ax[4] = {vx.x, vx.y, vx.z, vx.w};
-                const float v = group_sum8(part4(sn, ax));
-                if (l == x) mine = v;
+                v[s] = part4(sn, ax);
             }
+            const float mine = group_sum8x8(v);
             if (act && l < n) {
                 if (l != bi && ((alive >> l) & 1u)) D[l < bi ? pair_t(l, bi) : pair_t(bi, l)] = mine;
                 if (l != bj) D[l < bj ? pair_t(l, bj) : pair_t(bj, l)] = __uint_as_float(INF_BITS);
