@@ -393,14 +393,6 @@ __device__ __forceinline__ float group_sum8x8(float (&v)[8]) {
         for (int s = 0; s < h; s++) v[s] = v[s] + __shfl_xor_sync(0xffffffffu, v[s + h], h);
     return v[0];
 }
-__device__ __forceinline__ unsigned long long group_min8(unsigned long long v) {
-#pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
-        v = y < v ? y : v;
-    }
-    return v;
-}
 
 template <int K>
 __global__ void __launch_bounds__(QUAD_WARPS * 32, QUAD_MINB)
@@ -545,17 +537,27 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         const int np = nmax * (nmax - 1) / 2;
         for (int m = nmax; m > K; m--) {
             const bool act = valid && __popc(alive) > K;
-            unsigned long long best = ~0ull;
+            // lexicographic argmin (d, i, j) (D18) in two group reductions: the minimum d
+            // (distances are finite and >= 0, dead pairs +inf), then the least (i << 8 | j)
+            // among the pairs that attain it
+            float dr[4];
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 const int t = l + 8 * r;
-                if (t < np) {
-                    const unsigned long long key = ((unsigned long long)__float_as_uint(D[t]) << 32) | s_pair[t];
-                    best = key < best ? key : best;
-                }
+                dr[r] = t < np ? D[t] : __uint_as_float(INF_BITS);
             }
-            best = group_min8(best);
-            const int bi = (int)((best >> 8) & 0xff), bj = (int)(best & 0xff);
+            float dmin = fminf(fminf(dr[0], dr[1]), fminf(dr[2], dr[3]));
+#pragma unroll
+            for (int o = 4; o >= 1; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            unsigned code = 0xffffu;
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const int t = l + 8 * r;
+                if (t < np && dr[r] == dmin) code = min(code, (unsigned)s_pair[t]);
+            }
+#pragma unroll
+            for (int o = 4; o >= 1; o >>= 1) code = min(code, __shfl_xor_sync(0xffffffffu, code, o));
+            const int bi = (int)(code >> 8), bj = (int)(code & 0xff);
             if (act && l < 7) lobe[bi][l] += lobe[bj][l];   // exact moment merge (D15)
             __syncwarp();
             if (m == K + 1) {   // the last merge: nothing reads sigma or D afterwards
@@ -602,15 +604,15 @@ k_sggxh_quad(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             __syncwarp();
         }
         if (valid) {
-            int slot = 0;
-            for (int c = 0; c < n; c++) {
-                if (!((alive >> c) & 1u)) continue;
+            // hard parents keep exactly K lobes: the set bits of alive, in list order
+            unsigned a = alive;
+#pragma unroll
+            for (int slot = 0; slot < K; slot++) {
+                const int c = __ffs(a) - 1;
+                a &= a - 1u;
                 if (l < 7) pclacc[((uint64_t)p * K + slot) * 7 + l] = lobe[c][l];
-                slot++;
             }
-            for (int q = slot; q < K; q++)
-                if (l < 7) pclacc[((uint64_t)p * K + q) * 7 + l] = 0;
-            if (l == 0) pncl[p] = (uint8_t)slot;
+            if (l == 0) pncl[p] = (uint8_t)K;
         }
         __syncwarp();
     }
@@ -768,13 +770,14 @@ k_sggxh_warp(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
             __syncwarp();
         }
         // output: surviving lobes in list order (K slots exactly, since n > K)
-        int slot = 0;
-        for (int cc = 0; cc < n; cc++) {
-            if (!((alive >> cc) & 1ull)) continue;
+        unsigned long long a = alive;
+#pragma unroll
+        for (int slot = 0; slot < K; slot++) {
+            const int cc = __ffsll((long long)a) - 1;
+            a &= a - 1ull;
             if (lane < 7) pclacc[(p * K + slot) * 7 + lane] = list_[cc][lane];
-            slot++;
         }
-        if (lane == 0) pncl[p] = (uint8_t)slot;
+        if (lane == 0) pncl[p] = (uint8_t)K;
         __syncwarp();
     }
 }
@@ -927,13 +930,14 @@ k_sggxh_half(const uint32_t* __restrict__ list, const unsigned* __restrict__ cou
         }
         // output: surviving lobes in list order (K slots exactly, since n > K)
         if (valid) {
-            int slot = 0;
-            for (int cc = 0; cc < n; cc++) {
-                if (!((alive >> cc) & 1u)) continue;
+            unsigned a = alive;
+#pragma unroll
+            for (int slot = 0; slot < K; slot++) {
+                const int cc = __ffs(a) - 1;
+                a &= a - 1u;
                 if (l < 7) pclacc[(p * K + slot) * 7 + l] = H.lobe[cc][l];
-                slot++;
             }
-            if (l == 0) pncl[p] = (uint8_t)slot;
+            if (l == 0) pncl[p] = (uint8_t)K;
         }
         __syncwarp();
     }
