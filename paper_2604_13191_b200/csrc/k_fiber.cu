@@ -277,6 +277,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
     const uint64_t nbatch = (S + 31) / 32;
     const float PI_F = 3.14159274101257324f;   // 0x40490FDB
     const bool whole = sh.cell_lo == 0 && sh.cell_hi == (1ull << (3 * g.logN - sh.shift));   // unsharded
+    const bool seg16 = (reinterpret_cast<uintptr_t>(seg) & 15u) == 0;
     for (uint64_t batch = blockIdx.x * (uint64_t)EMIT_WARPS + wib; batch < nbatch;
          batch += (uint64_t)gridDim.x * EMIT_WARPS) {
         const uint64_t p = batch * 32 + lane;
@@ -284,9 +285,25 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
         Fib f;
         float d[3] = {0, 0, 0};
         float rg = 0.0f;
+        // the batch's primitive tile (32 segments x 24 contiguous bytes) staged in the (empty)
+        // survivor FIFO with 16-byte coalesced loads when the array is 16-byte aligned, then read
+        // as 6 words per lane (measured neutral against 6 strided 4-byte loads per lane: the
+        // kernel is issue-bound on the predicate)
+        {
+            float* st = reinterpret_cast<float*>(s_q[wib]);
+            const uint64_t p0 = batch * 32;
+            const int ns = S - p0 < 32 ? (int)(S - p0) : 32;
+            if (seg16 && ns == 32) {
+                const float4* src = reinterpret_cast<const float4*>(seg + 6 * p0);
+                for (int w = lane; w < 48; w += 32) reinterpret_cast<float4*>(st)[w] = src[w];
+            } else {
+                for (int w = lane; w < 6 * ns; w += 32) st[w] = seg[6 * p0 + w];
+            }
+            __syncwarp();
+        }
         if (p < S) {
             float s[6];
-            for (int q = 0; q < 6; q++) s[q] = seg[6 * p + q];
+            for (int q = 0; q < 6; q++) s[q] = reinterpret_cast<const float*>(s_q[wib])[6 * lane + q];
             SegGeom G;
             seg_geom(g, s, rad[p], G);
             rg = G.rg;
@@ -322,6 +339,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
             s_f[wib][15][lane] = rg;
             far_consts(f.w, rg, s_f[wib][16][lane], s_f[wib][17][lane]);
         }
+        __syncwarp();   // every lane has read its segment from the staging words
         // warp inclusive scan of the candidate counts
         uint32_t incl = cnt;
         for (int o = 1; o < 32; o <<= 1) {
