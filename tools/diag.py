@@ -6,6 +6,8 @@
     python tools/diag.py maxsize [segments] [N]    config 5 point: device time, counts, memory
     python tools/diag.py density [segments]        device time of the sub-voxel density pass (NEXT-2)
     python tools/diag.py overlap [parts]           config 4 as Morton parts on concurrent streams (host threads)
+    python tools/diag.py copies  [priority]        e2e step timeline: when each level's D2H starts / ends on the copy stream
+    python tools/diag.py e2e     [steps]           e2e loop of config 4, steps synchronised vs pipelined, copy-stream priority 0 / -1
 """
 import os
 import sys
@@ -148,6 +150,124 @@ def overlap(parts=2):
         t3 = time.perf_counter()
         print(f"whole {1e3 * (t1 - t0):.1f} ms | {parts} shards sequential {1e3 * (t2 - t1):.1f} ms | "
               f"concurrent {1e3 * (t3 - t2):.1f} ms", flush=True)
+
+
+def copies(priority=-1):
+    """One e2e step of config 4 (host buffers, all 13 levels copied back as bench.py does), with
+    events on the main and the copy stream: when each level is built and when its D2H starts and
+    lands, in ms from the step's start."""
+    c = gen.config(4)
+    pa = torch.from_numpy(c["segments"]).pin_memory()
+    pb = torch.from_numpy(c["radii"]).pin_memory()
+    cs = torch.cuda.Stream(priority=int(priority))
+    main = torch.cuda.current_stream()
+    host = {}
+
+    def ev(s):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(s)
+        return e
+
+    for it in range(3):
+        marks = []
+        t0 = ev(main)
+        v = Vox(c["grid_res"], c["bbox"])
+        v.voxelize_fibers_host(pa, pb)
+        for l in range(0, c["levels"] + 1):
+            if l > 0:
+                v.build_lod(l)
+            n = v.size(l)
+            if l not in host:
+                host[l] = {"key": torch.empty(n, dtype=torch.int64).pin_memory(),
+                           "mass": torch.empty(n, dtype=torch.float32).pin_memory(),
+                           "m6": torch.empty(6 * n, dtype=torch.float32).pin_memory()}
+                if l > 0:
+                    host[l]["ncl"] = torch.empty(n, dtype=torch.uint8).pin_memory()
+                    host[l]["cl"] = torch.empty(n * 21, dtype=torch.float32).pin_memory()
+            built = ev(main)
+            b = ev(cs)
+            v.copy_level_async(l, host[l], cs)
+            e = ev(cs)
+            marks.append((l, n, built, b, e))
+        cs.synchronize()
+        torch.cuda.synchronize()
+        v.close()
+        if it == 2:
+            for l, n, built, b, e in marks:
+                byt = n * (36 + (85 if l > 0 else 0))
+                print(f"level {l:2d} n={n:10d} built {t0.elapsed_time(built):7.1f}  d2h queued-after "
+                      f"{t0.elapsed_time(b):7.1f} .. landed {t0.elapsed_time(e):7.1f} ms  "
+                      f"({byt / 1e9:.2f} GB, {byt / 1e6 / max(b.elapsed_time(e), 1e-3):.1f} GB/s)", flush=True)
+
+
+def e2e(steps=5):
+    c = gen.config(4)
+    pa = torch.from_numpy(c["segments"]).pin_memory()
+    pb = torch.from_numpy(c["radii"]).pin_memory()
+    main = torch.cuda.current_stream()
+    host = {}
+    L = c["levels"]
+
+    def run(pipelined, prio):
+        cs = torch.cuda.Stream(priority=prio)
+        pend = []
+
+        def step():
+            v = Vox(c["grid_res"], c["bbox"])
+            v.voxelize_fibers_host(pa, pb)
+            for l in range(0, L + 1):
+                if l > 0:
+                    v.build_lod(l)
+                n = v.size(l)
+                if l not in host:
+                    host[l] = {"key": torch.empty(n, dtype=torch.int64).pin_memory(),
+                               "mass": torch.empty(n, dtype=torch.float32).pin_memory(),
+                               "m6": torch.empty(6 * n, dtype=torch.float32).pin_memory()}
+                    if l > 0:
+                        host[l]["ncl"] = torch.empty(n, dtype=torch.uint8).pin_memory()
+                        host[l]["cl"] = torch.empty(n * 21, dtype=torch.float32).pin_memory()
+                v.copy_level_async(l, host[l], cs)
+            if pipelined:
+                e = torch.cuda.Event()
+                e.record(cs)
+                while pend:
+                    pv, pe = pend.pop(0)
+                    pe.synchronize()
+                    pv.close()
+                pend.append((v, e))
+            else:
+                cs.synchronize()
+                v.close()
+
+        step()
+        while pend:
+            pv, pe = pend.pop(0)
+            pe.synchronize()
+            pv.close()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(main)
+        for _ in range(int(steps)):
+            step()
+        if pend:
+            last = pend[-1][1]
+            while pend:
+                pv, pe = pend.pop(0)
+                pe.synchronize()
+                pv.close()
+            main.wait_event(last)
+        e1.record(main)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / int(steps)
+        print(f"pipelined={pipelined} priority={prio}: {ms:.1f} ms/step (events), "
+              f"{1e3 * (time.perf_counter() - t0) / int(steps):.1f} ms/step (wall), "
+              f"{c['segments'].shape[0] / ms / 1e3:.1f} M segments/s", flush=True)
+
+    for pipelined in (False, True):
+        for prio in (0, -1):
+            run(pipelined, prio)
 
 
 if __name__ == "__main__":
