@@ -202,6 +202,9 @@ vox_status vox_encode_level(vox_ctx* ctx, uint32_t level, uint8_t* sggx6, uint8_
  * the ctx. The fp32 values are formed from the accumulators by a small kernel on `stream`
  * into stream-ordered scratch from the device pool (allocated and freed on `stream`) before
  * each D2H; a level whose views an earlier read formed is copied from them, after that read.
+ * Those kernels share the SMs with the build still running on the ctx stream: give `stream`
+ * a high priority (cudaStreamCreateWithPriority) so they are scheduled ahead of the build's
+ * blocks and the copy engine is not left idle behind them (bench.py does).
  * Level 0 supports key / mass / m6 only (ncl or cl non-NULL -> VOX_ERR_INVALID_ARG). */
 vox_status vox_copy_level_async(vox_ctx* ctx, uint32_t level, uint64_t* key, float* mass, float* m6,
                                 uint8_t* ncl, float* cl, void* stream);
