@@ -553,26 +553,32 @@ k_fiber_density(const float* __restrict__ seg, const float* __restrict__ rad, ui
                 // (this classifier is conservative geometry, not the pinned predicate: fused
                 // multiply-adds are fine here, their rounding is far inside the 0.1 margin)
                 const float pa = __fmaf_rn(e1a, d8[1], e0 * d8[0]), pb = __fmaf_rn(e1b, d8[1], e0 * d8[0]);
+                const unsigned lt = (1u << lane) - 1u;
+                const unsigned tag = ((unsigned)slot << 9) | (unsigned)lane;   // sub-voxel lane + 32 q
+                // rows q = 2 qz + h: z offset qz, y offset (lane >> 3) + 4 h (the two y values unrolled)
 #pragma unroll 1
-                for (int q = 0; q < 16; q++) {
-                    const int sub = lane + 32 * q;
-                    const float e1 = (q & 1) ? e1b : e1a, e2 = e2b + (float)(q >> 1);
-                    float t = __fmaf_rn(e2, d8[2], (q & 1) ? pb : pa) * iww8;
-                    t = fminf(fmaxf(t, 0.0f), 1.0f);
-                    const float q0 = __fmaf_rn(-t, d8[0], e0), q1 = __fmaf_rn(-t, d8[1], e1),
-                                q2 = __fmaf_rn(-t, d8[2], e2);
-                    const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f),
-                                o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
-                    const float box2 = __fmaf_rn(o0, o0, __fmaf_rn(o1, o1, o2 * o2));
-                    const float c2 = __fmaf_rn(q0, q0, __fmaf_rn(q1, q1, q2 * q2));
-                    const bool sure = box2 < near2, open = !sure && !(c2 > far2);
-                    const unsigned bs = __ballot_sync(0xffffffffu, sure);
-                    const unsigned bo = __ballot_sync(0xffffffffu, open);
-                    if (lane == 0) s_m[wib][slot][q] = bs;
-                    if (open)
-                        s_q[wib][(tail + __popc(bo & ((1u << lane) - 1u))) & (DENS_RING - 1)] =
-                            (uint16_t)((slot << 9) | sub);
-                    tail += __popc(bo);
+                for (int qz = 0; qz < 8; qz++) {
+                    const float e2 = e2b + (float)qz;
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int q = 2 * qz + h;
+                        const float e1 = h ? e1b : e1a;
+                        float t = __fmaf_rn(e2, d8[2], h ? pb : pa) * iww8;
+                        t = fminf(fmaxf(t, 0.0f), 1.0f);
+                        const float q0 = __fmaf_rn(-t, d8[0], e0), q1 = __fmaf_rn(-t, d8[1], e1),
+                                    q2 = __fmaf_rn(-t, d8[2], e2);
+                        const float o0 = fmaxf(fabsf(q0) - 0.5f, 0.0f), o1 = fmaxf(fabsf(q1) - 0.5f, 0.0f),
+                                    o2 = fmaxf(fabsf(q2) - 0.5f, 0.0f);
+                        const float box2 = __fmaf_rn(o0, o0, __fmaf_rn(o1, o1, o2 * o2));
+                        const float c2 = __fmaf_rn(q0, q0, __fmaf_rn(q1, q1, q2 * q2));
+                        const bool sure = box2 < near2, open = !sure && !(c2 > far2);
+                        const unsigned bs = __ballot_sync(0xffffffffu, sure);
+                        const unsigned bo = __ballot_sync(0xffffffffu, open);
+                        if (lane == 0) s_m[wib][slot][q] = bs;
+                        if (open)
+                            s_q[wib][(tail + __popc(bo & lt)) & (DENS_RING - 1)] = (uint16_t)(tag + 32u * q);
+                        tail += __popc(bo);
+                    }
                 }
                 __syncwarp();
             }
