@@ -120,7 +120,11 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
             bp[2 * ax] = (u[ax] > 0.0f && u[ax] < 1.0f) ? u[ax] : 2.0f;
             bp[2 * ax + 1] = (v[ax] > 0.0f && v[ax] < 1.0f) ? v[ax] : 2.0f;
         } else {
-            u[ax] = v[ax] = Wu[ax] = Wuu[ax] = Wv[ax] = Wvv[ax] = 0.0f;
+            // a fixed axis takes the u >= H branch below with w = Wu = Wuu = 0: adding +0 leaves
+            // A, B, C bit-identical to skipping the axis (none of them is ever -0), so the piece
+            // loop needs no per-axis moving test
+            u[ax] = v[ax] = 2.0f;
+            Wu[ax] = Wuu[ax] = Wv[ax] = Wvv[ax] = 0.0f;
             float c = 0.0f;
             if (f.a[ax] < lo[ax]) c = lo[ax] - f.a[ax];
             else if (f.a[ax] > hi[ax]) c = f.a[ax] - hi[ax];
@@ -146,7 +150,6 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
         float A = 0.0f, B = 0.0f, C = C0;
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
-            if (!(f.moving & (1u << ax))) continue;
             if (u[ax] >= H) { A = A + f.w[ax]; B = B + Wu[ax]; C = C + Wuu[ax]; }
             else if (v[ax] <= L) { A = A + f.w[ax]; B = B + Wv[ax]; C = C + Wvv[ax]; }
         }
