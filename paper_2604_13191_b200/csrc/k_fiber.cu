@@ -93,7 +93,7 @@ struct Fib {
     unsigned moving;   // bit ax set iff w_ax > 0
 };
 
-// Sorting network for 6 values (ascending); values outside (0,1) were replaced by 2.
+// Sorting network for 6 values (ascending); values outside (0,1) were replaced by 1.
 __device__ __forceinline__ void cswap(float& x, float& y) {
     float lo = pmin(x, y), hi = pmax(x, y);
     x = lo; y = hi;
@@ -117,8 +117,10 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
             Wuu[ax] = Wu[ax] * u[ax];
             Wv[ax] = f.w[ax] * v[ax];
             Wvv[ax] = Wv[ax] * v[ax];
-            bp[2 * ax] = (u[ax] > 0.0f && u[ax] < 1.0f) ? u[ax] : 2.0f;
-            bp[2 * ax + 1] = (v[ax] > 0.0f && v[ax] < 1.0f) ? v[ax] : 2.0f;
+            // breakpoints outside (0, 1) become 1.0: sorted behind the interior ones, so the
+            // piece ends are H_p = bp[p] for every piece p <= m (the last one ends at 1)
+            bp[2 * ax] = (u[ax] > 0.0f && u[ax] < 1.0f) ? u[ax] : 1.0f;
+            bp[2 * ax + 1] = (v[ax] > 0.0f && v[ax] < 1.0f) ? v[ax] : 1.0f;
         } else {
             // a fixed axis takes the u >= H branch below with w = Wu = Wuu = 0: adding +0 leaves
             // A, B, C bit-identical to skipping the axis (none of them is ever -0), so the piece
@@ -129,7 +131,7 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
             if (f.a[ax] < lo[ax]) c = lo[ax] - f.a[ax];
             else if (f.a[ax] > hi[ax]) c = f.a[ax] - hi[ax];
             C0 = C0 + c * c;
-            bp[2 * ax] = bp[2 * ax + 1] = 2.0f;
+            bp[2 * ax] = bp[2 * ax + 1] = 1.0f;
         }
     }
     // optimal 12-comparator network for 6 inputs
@@ -146,7 +148,7 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
     for (int p = 0; p < 7; p++) {
         if (p > m) break;
         const float L = p == 0 ? 0.0f : bp[p - 1];
-        const float H = p < m ? bp[p] : 1.0f;
+        const float H = p < 6 ? bp[p] : 1.0f;   // compile-time p: bp[m] = 1 when m < 6
         float A = 0.0f, B = 0.0f, C = C0;
 #pragma unroll
         for (int ax = 0; ax < 3; ax++) {
@@ -168,8 +170,12 @@ __device__ __forceinline__ bool fiber_key(const Fib& f, int64_t i, int64_t j, in
             hi_m = pmin(t2, H);
             if (!(lo_m <= hi_m)) continue;
         }
-        if (!found) { ta = lo_m; tb = hi_m; found = true; }
-        else { ta = pmin(ta, lo_m); tb = pmax(tb, hi_m); }
+        // pieces are ordered and lo >= L, hi <= H inside a piece, so over the feasible pieces
+        // min lo is the first one's lo and max hi the last one's hi (the pinned pmin / pmax
+        // would return exactly these values)
+        if (!found) ta = lo_m;
+        tb = hi_m;
+        found = true;
     }
     if (!found) return false;
     ell = f.len * (tb - ta);
