@@ -253,11 +253,34 @@ __device__ __forceinline__ uint64_t tri_upper(const unsigned long long* __restri
 
 // Warps take TRI_CHUNK consecutive candidates of the global (triangle-major) candidate space;
 // each lane locates its triangle by a binary search bounded by the chunk's first/last triangle.
-// Keys (SAT, §6) emit (key, prim | clipped area (§7)) pairs into their bins.
+// Keys (SAT, §6) in the shard go to a per-warp FIFO in candidate order; the clipped area (§7)
+// is evaluated 32 queued keys at a time (full warps: about a quarter of the candidates are
+// keys, so evaluating them in place left three lanes in four idle), then the (key, prim |
+// area) pairs are appended to their bins.
+__device__ __forceinline__ void tri_eval_queue(const int4* q, int nq, int lane, const TriSetup* __restrict__ ts,
+                                               const Bins& bins, uint64_t* __restrict__ keys,
+                                               uint64_t* __restrict__ vals, unsigned* __restrict__ flags) {
+    bool emit = false;
+    uint64_t mkey = 0, val = 0;
+    if (lane < nq) {
+        const int4 e = q[lane];
+        float g[9];
+#pragma unroll
+        for (int x = 0; x < 9; x++) g[x] = ts[e.x].g[x];
+        const float A = tri_clip_area(g, e.y, e.z, e.w);
+        mkey = morton3((uint32_t)e.y, (uint32_t)e.z, (uint32_t)e.w);
+        val = (uint64_t)(uint32_t)e.x | ((uint64_t)__float_as_uint(A) << 32);
+        emit = true;
+    }
+    if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(TRI_WARPS * 32)
 k_tri_emit(const TriSetup* __restrict__ ts, const unsigned long long* __restrict__ toff, uint64_t T, GridXf gx,
            Shard sh, Bins bins, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals,
            unsigned* __restrict__ flags) {
+    __shared__ int4 s_q[TRI_WARPS][64];   // key FIFO: (triangle, i, j, k)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const unsigned long long total = toff[T];
     const unsigned long long nchunk = (total + TRI_CHUNK - 1) / TRI_CHUNK;
@@ -272,10 +295,11 @@ k_tri_emit(const TriSetup* __restrict__ ts, const unsigned long long* __restrict
         }
         tlo = __shfl_sync(0xffffffffu, tlo, 0);
         thi = __shfl_sync(0xffffffffu, thi, 0);
+        int qn = 0;
         for (unsigned long long c0 = cb; c0 < ce; c0 += 32) {
             const unsigned long long c = c0 + lane;
-            bool emit = false;
-            uint64_t mkey = 0, val = 0;
+            bool key = false;
+            int4 ent = make_int4(0, 0, 0, 0);
             if (c < ce) {
                 const uint64_t t = tri_upper(toff, tlo, thi, c);
                 const TriSetup s = ts[t];
@@ -285,16 +309,24 @@ k_tri_emit(const TriSetup* __restrict__ ts, const unsigned long long* __restrict
                 const int64_t j = s.e0[1] + (int64_t)(q % s.ey);
                 const int64_t k = s.e0[2] + (int64_t)(q / s.ey);
                 if (tri_box_sat(s.g, i, j, k)) {
-                    mkey = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k);
-                    const uint64_t cell = mkey >> sh.shift;
-                    if (cell >= sh.cell_lo && cell < sh.cell_hi) {
-                        const float A = tri_clip_area(s.g, i, j, k);
-                        emit = true;
-                        val = t | ((uint64_t)__float_as_uint(A) << 32);
-                    }
+                    const uint64_t cell = morton3((uint32_t)i, (uint32_t)j, (uint32_t)k) >> sh.shift;
+                    key = cell >= sh.cell_lo && cell < sh.cell_hi;
+                    ent = make_int4((int)t, (int)i, (int)j, (int)k);
                 }
             }
-            if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
+            const unsigned bal = __ballot_sync(0xffffffffu, key);
+            if (key) s_q[wib][qn + __popc(bal & ((1u << lane) - 1u))] = ent;   // qn < 32 here: < 64
+            qn += __popc(bal);
+            __syncwarp();
+            // the one evaluation site of the clipped area: full rounds, after the last chunk the rest
+            const bool last = c0 + 32 >= ce;
+            while (qn >= 32 || (last && qn > 0)) {
+                const int m = qn < 32 ? qn : 32;
+                tri_eval_queue(s_q[wib], m, lane, ts, bins, keys, vals, flags);
+                if (lane < qn - m) s_q[wib][lane] = s_q[wib][m + lane];
+                qn -= m;
+                __syncwarp();
+            }
         }
     }
 }
