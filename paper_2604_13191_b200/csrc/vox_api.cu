@@ -271,6 +271,11 @@ static vox_status ensure_dev(vox_ctx* c) {
     CKS(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = UINT64_MAX;
     CKS(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // no hidden cross-stream waits: memory freed on an async-copy stream (the fp32-view
+    // scratch of vox_copy_level_async) must not be handed to the ctx stream by making it wait
+    // for that stream -- the build would stall behind the D2H. Completed frees are still reused.
+    int no_dep = 0;
+    CKS(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no_dep));
     CKS(cudaMallocAsync((void**)&c->d_flags, 16, c->stream));
     CKS(cudaMallocAsync((void**)&c->d_counter, 16, c->stream));
     CKS(cudaMallocAsync((void**)&c->d_lodwork, 32, c->stream));
