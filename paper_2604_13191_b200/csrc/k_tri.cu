@@ -264,12 +264,13 @@ __device__ __forceinline__ void tri_eval_queue(const int4* q, int nq, int lane, 
     uint64_t mkey = 0, val = 0;
     if (lane < nq) {
         const int4 e = q[lane];
+        const uint32_t t = (uint32_t)e.x;   // prim indices are 32-bit (the pair value packs them so)
         float g[9];
 #pragma unroll
-        for (int x = 0; x < 9; x++) g[x] = ts[e.x].g[x];
+        for (int x = 0; x < 9; x++) g[x] = ts[t].g[x];
         const float A = tri_clip_area(g, e.y, e.z, e.w);
         mkey = morton3((uint32_t)e.y, (uint32_t)e.z, (uint32_t)e.w);
-        val = (uint64_t)(uint32_t)e.x | ((uint64_t)__float_as_uint(A) << 32);
+        val = (uint64_t)t | ((uint64_t)__float_as_uint(A) << 32);
         emit = true;
     }
     if (__ballot_sync(0xffffffffu, emit)) append_binned(emit, mkey, val, lane, bins, keys, vals, flags);
