@@ -213,6 +213,19 @@ def _cpu_model():
     return None
 
 
+def _config_of(args, n_prims, N, levels, world, fib=True):
+    """The bench line's `config` (shared by both arms, so the driver compares like with like)."""
+    return {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config]
+                        + (f" [point: {n_prims} segments at {N}^3]" if args.config == 5 else ""),
+            "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
+            "front_end": (f"sampled ({args.sampled} samples per Catmull-Rom piece)" if fib else
+                          f"sampled (budget {args.sampled} per largest triangle)") if args.sampled
+            else "exact overlap",
+            "sggxh_distance": args.distance if args.distance == "sigma"
+            else f"hist (N={args.hist_samples} samples, 5x5x5 bins, sliced W1)",
+            "l2": "inputs (28 B x prims) larger than L2; no flush"}
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores, bounded samples."""
     c = _workload(args.config, args.segments)
@@ -230,10 +243,14 @@ def run_reference(args):
             times.append(dt)
             counts.append(n)
     value = sum(counts) / sum(times)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "segments/s", "n_gpus": 0,
+    # the same `config` as our arm (the workload the value is quoted on); the sample each step
+    # actually ran is in cpu_baseline.sample
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "segments/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": f"config {args.config} sample: {desc}"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": _config_of(args, int(c["segments"].shape[0]), c["grid_res"], c["levels"], world),
             "cpu_baseline": {"value": value, "unit": "segments/s", "cores": thr, "kind": "oracle", "sample": desc,
                              "host_cpus": ncpu, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "segments/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -451,15 +468,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "segments/s" if fib else "triangles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"config {args.config}: " + __import__("gen").CONFIGS[args.config]
-                       + (f" [point: {n_prims} segments at {N}^3]" if args.config == 5 else ""),
-                       "prims": n_prims, "grid_res": N, "levels": levels, "parallelism": f"morton{world}",
-                       "front_end": (f"sampled ({args.sampled} samples per Catmull-Rom piece)" if fib else
-                                     f"sampled (budget {args.sampled} per largest triangle)") if args.sampled
-                       else "exact overlap",
-                       "sggxh_distance": args.distance if args.distance == "sigma"
-                       else f"hist (N={args.hist_samples} samples, 5x5x5 bins, sliced W1)",
-                       "l2": "inputs (28 B x prims) larger than L2; no flush"},
+            "config": _config_of(args, n_prims, N, levels, world, fib),
             "lod_ms": stage["ms_total_lod"], "vox_ms": stage["ms_total_vox"],
             "hbm_alg_gbs_full_build": (bytes_vox + bytes_lod) / (ms_step / 1e3) / 1e9,
             "stages_ms": {k2: round(v2, 4) for k2, v2 in stage.items()},
