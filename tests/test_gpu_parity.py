@@ -186,6 +186,55 @@ def test_host_entry_points(P):
         assert np.array_equal(outs[l]["ncl"].numpy(), r["ncl"]) and np.array_equal(outs[l]["cl"].numpy(), r["cl"])
 
 
+def test_overlapped_contexts_async_copies(P):
+    """The e2e pattern of bench.py: consecutive jobs whose contexts overlap -- job i's level
+    copies (vox_copy_level_async on a high-priority side stream, fp32 views formed there) are
+    still in flight while job i+1 uploads from host buffers and builds -- each job's host
+    results equal the oracle's, bit for bit."""
+    c = gen.config(2)
+    N, L = c["grid_res"], c["levels"]
+    o = oracle.Oracle(N, c["bbox"])
+    o.add_fibers(c["segments"], c["radii"])
+    o.build(L)
+    pa = torch.from_numpy(c["segments"]).pin_memory()
+    pb = torch.from_numpy(c["radii"]).pin_memory()
+    side = torch.cuda.Stream(priority=-1)
+    jobs = []
+    for _ in range(3):
+        v = P.Vox(N, c["bbox"])
+        v.voxelize_fibers_host(pa, pb)
+        outs = {}
+        for l in range(L + 1):
+            if l:
+                v.build_lod(l)
+            n = v.size(l)
+            outs[l] = {"key": torch.empty(n, dtype=torch.int64).pin_memory(),
+                       "mass": torch.empty(n, dtype=torch.float32).pin_memory(),
+                       "m6": torch.empty((n, 6), dtype=torch.float32).pin_memory()}
+            if l:
+                outs[l]["ncl"] = torch.empty(n, dtype=torch.uint8).pin_memory()
+                outs[l]["cl"] = torch.empty((n, 3, 7), dtype=torch.float32).pin_memory()
+            v.copy_level_async(l, outs[l], side)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        jobs.append((v, ev, outs))
+        if len(jobs) > 1:   # release the previous job once its copies have landed
+            pv, pe, _ = jobs[-2]
+            pe.synchronize()
+            pv.close()
+    jobs[-1][1].synchronize()
+    jobs[-1][0].close()
+    for _, _, outs in jobs:
+        for l in range(L + 1):
+            r = o.level(l)
+            assert np.array_equal(outs[l]["key"].numpy().astype(np.uint64), r["key"]), l
+            assert np.array_equal(outs[l]["mass"].numpy(), r["mass"]), l
+            assert np.array_equal(outs[l]["m6"].numpy(), r["m6"]), l
+            if l:
+                assert np.array_equal(outs[l]["ncl"].numpy(), r["ncl"]), l
+                assert np.array_equal(outs[l]["cl"].numpy(), r["cl"]), l
+
+
 def test_errors_and_states(P):
     v = P.Vox(64, [0, 0, 0, 1, 1, 1])
     bad = torch.tensor([[[0.1, 0.1, 0.1], [0.2, float("nan"), 0.2]]], device="cuda")
