@@ -218,15 +218,6 @@ __device__ __forceinline__ uint32_t div_magic(uint32_t x, uint32_t d, uint32_t m
     if (x - q * d >= d) q++;
     return q;
 }
-// §2 Morton key from a shared 256-entry table of 8-bit bit spreads (grid coordinates < 2^16:
-// two lookups per axis) -- the same bits as morton3, a quarter of its 64-bit shift/mask steps.
-__device__ __forceinline__ uint64_t morton3_tab(const uint64_t* __restrict__ tab, uint32_t i, uint32_t j, uint32_t k) {
-    const uint64_t x = tab[i & 255u] | (tab[(i >> 8) & 255u] << 24);
-    const uint64_t y = tab[j & 255u] | (tab[(j >> 8) & 255u] << 24);
-    const uint64_t z = tab[k & 255u] | (tab[(k >> 8) & 255u] << 24);
-    return x | (y << 1) | (z << 2);
-}
-
 // Evaluates the first nq (<= 32) queued candidates, one per lane: the pinned predicate and
 // l_r (§4), the exact S_acc contribution (segmented scan over lanes: queue order keeps the
 // owner segments non-decreasing) and the binned append of in-grid, in-shard keys.
@@ -296,8 +287,7 @@ k_fiber_emit(const float* __restrict__ seg, const float* __restrict__ rad, uint6
     const float PI_F = 3.14159274101257324f;   // 0x40490FDB
     const bool whole = sh.cell_lo == 0 && sh.cell_hi == (1ull << (3 * g.logN - sh.shift));   // unsharded
     __shared__ uint64_t s_mtab[256];   // 8-bit Morton spreads
-    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_mtab[t] = spread3((uint32_t)t);
-    __syncthreads();
+    mtab_init(s_mtab);
     const bool seg16 = (reinterpret_cast<uintptr_t>(seg) & 15u) == 0;
     for (uint64_t batch = blockIdx.x * (uint64_t)EMIT_WARPS + wib; batch < nbatch;
          batch += (uint64_t)gridDim.x * EMIT_WARPS) {

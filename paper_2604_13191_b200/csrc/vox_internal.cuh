@@ -88,6 +88,19 @@ __host__ __device__ __forceinline__ uint64_t spread3(uint32_t v) {
 __host__ __device__ __forceinline__ uint64_t morton3(uint32_t i, uint32_t j, uint32_t k) {
     return spread3(i) | (spread3(j) << 1) | (spread3(k) << 2);
 }
+// §2 Morton key from a shared 256-entry table of 8-bit bit spreads (coordinates < 2^16: two
+// lookups per axis) -- the same bits as morton3 with a quarter of its 64-bit shift/mask steps.
+// mtab_init fills the table (whole block, then a barrier: call it before any divergence).
+__device__ __forceinline__ uint64_t morton3_tab(const uint64_t* __restrict__ tab, uint32_t i, uint32_t j, uint32_t k) {
+    const uint64_t x = tab[i & 255u] | (tab[(i >> 8) & 255u] << 24);
+    const uint64_t y = tab[j & 255u] | (tab[(j >> 8) & 255u] << 24);
+    const uint64_t z = tab[k & 255u] | (tab[(k >> 8) & 255u] << 24);
+    return x | (y << 1) | (z << 2);
+}
+__device__ __forceinline__ void mtab_init(uint64_t* tab) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) tab[t] = spread3((uint32_t)t);
+    __syncthreads();
+}
 __host__ __device__ __forceinline__ uint32_t compact3(uint64_t x) {
     x &= 0x1249249249249249ull;
     x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
