@@ -99,7 +99,10 @@ typedef struct {
  * grid_res: power of two in [2, 8192] (D27) else VOX_ERR_INVALID_ARG.
  * bbox: host float[6] = min xyz, max xyz; must be finite with max > min per axis
  * (else VOX_ERR_DEGENERATE_BBOX). opt: host pointer or NULL (defaults). No device
- * allocation happens here. */
+ * allocation happens here. The first call that touches the device configures the device's
+ * default memory pool process-wide: release threshold unlimited (freed stream-ordered memory
+ * stays mapped for the next call) and no internal cross-stream dependencies (memory freed on
+ * one stream is not handed to another by making it wait; completed frees are still reused). */
 vox_status vox_create(vox_ctx** out, uint32_t grid_res, const float bbox[6], const vox_options* opt);
 
 /* Voxelize S fiber segments (capsules; PREDICATES §3-§5, north star).
