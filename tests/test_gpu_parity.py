@@ -83,6 +83,41 @@ def test_random_fibers_ragged(P, seed, n, N, rscale):
         _cmp_level(v.level(l), o.level(l), l, f"fibers{seed}")
 
 
+def test_fibers_on_grid_planes_and_axes(P):
+    """Adversarial fibers for the pinned predicate's branches (PREDICATES §4): axis-aligned
+    segments (one or two fixed axes), endpoints exactly on voxel faces / corners (slab
+    parameters exactly 0 or 1), lines at exactly r = 1/2 voxel from a row of voxel faces
+    (tangent keys), diagonals through corners, spheres on corners; all levels bit-exact."""
+    N = 64
+    h = 1.0 / N
+    segs, radii = [], []
+    for ax in range(3):   # along each axis: on a grid line, on a face, inside; r tangent or not
+        for off, r in ((0.0, 0.5), (0.5, 0.5), (0.25, 0.5), (0.0, 0.25), (0.5, 1.0), (0.3, 0.0)):
+            a = np.array([20.0, 30.0, 40.0]) + off
+            b = a.copy()
+            b[ax] += 7.0
+            segs.append([a * h, b * h])
+            radii.append(r * h)
+    for d in ((1, 1, 0), (1, 1, 1), (2, 1, 0), (0, 1, 1)):   # through corners, two or one fixed axes
+        a = np.array([10.0, 12.0, 14.0])
+        b = a + 5.0 * np.array(d, float)
+        for r in (0.5, 0.7071067811865476, 0.25):
+            segs.append([a * h, b * h])
+            radii.append(r * h)
+    for c in ((8.0, 8.0, 8.0), (8.5, 8.0, 8.0), (63.0, 63.0, 63.0), (0.0, 0.0, 0.0)):   # spheres
+        p = np.array(c) * h
+        segs.append([p, p])
+        radii.append(0.5 * h)
+        segs.append([p, p + np.array([0.0, 0.0, 1.0]) * h])   # unit segment from a corner
+        radii.append(0.5 * h)
+    segs = np.asarray(segs, np.float32)
+    radii = np.asarray(radii, np.float32)
+    L = int(np.log2(N))
+    v, o = _run_both(P, N, [0, 0, 0, 1, 1, 1], L, segs=segs, radii=radii)
+    for l in range(L + 1):
+        _cmp_level(v.level(l), o.level(l), l, "grid-planes")
+
+
 def test_triangles_tangent_mode_and_k(P):
     t, d = gen.ridge_mesh(n_quads=40, ridges=10, height=4 / 256, noise_amp=0.5 / 256)
     for k in (1, 2, 3, 8):
